@@ -1,0 +1,210 @@
+/*
+ * heightcast.h -- C ABI of libheightcast_cuda.so, the sm_100a hot path of the
+ * two-step adaptive-heightfield renderer (arXiv 2201.10887).
+ *
+ * The reference (pkg/src/heightcast, CPU Python) has one native seam, the Numba
+ * kernel `_kernels.traverse_batch` called from `render._batch_traverse`
+ * (render.py:141-145); everything else is numpy called from the Python API
+ * (`render_frame`, `discretize_cascade`, `build_max_mipmap`, ...).  This ABI
+ * replaces that seam one-for-one (`hc_traverse_batch`) and adds the fused
+ * per-frame kernels that the Python drop-in (paper_2201_10887_b200/) calls in
+ * place of the numpy stages.  Each entry point names the reference code it
+ * replaces.
+ *
+ * Conventions (all entry points):
+ *   - every pointer is a DEVICE pointer owned by the caller (torch tensors); the
+ *     library never allocates and keeps no global mutable state except the
+ *     thread-local error message;
+ *   - every call is asynchronous on the caller's `stream` (a cudaStream_t);
+ *   - return HC_OK (0) or a negative HC_E* code; hc_last_error() explains it;
+ *   - descriptor structs are passed by host pointer and copied into kernel
+ *     parameters, so calls are CUDA-graph capturable.
+ * Float64 paths (mask, rays, traversal, resolve, shading) evaluate the
+ * reference's expressions in the reference's order with no FMA contraction and
+ * IEEE division/sqrt, so they are bit-identical to the reference on identical
+ * rasters.  Discretization (Eq. 1/2) runs in float32 with tile-local anchored
+ * coordinates (tolerance-matched).
+ */
+#ifndef HEIGHTCAST_H
+#define HEIGHTCAST_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HC_ABI_VERSION 1
+#define HC_MAX_EDGES 32      /* polygon edges per cascade mask          */
+#define HC_MAX_CASCADES 8    /* K (the reference hard-codes 3)           */
+#define HC_MAX_LEVELS 20     /* max-mip levels (R <= 2^19)               */
+
+enum {
+    HC_OK = 0,
+    HC_EINVAL = -1,          /* bad argument (sizes, null pointers, K)   */
+    HC_ECUDA = -2,           /* CUDA launch/runtime error                */
+    HC_ECAPACITY = -3        /* caller-provided buffer too small          */
+};
+
+typedef void *hc_stream_t;   /* cudaStream_t */
+
+/* Device-resident adaptive grid + influence table.
+ * grid.py:79-210 (SoA arrays, int32 min-cell tile index, -1 = hole) and
+ * grid.py:350-434 (CSR influence lists, ascending, int32 on the device).
+ * `rec4`/`rec_dd` are the anchored influence records built once per
+ * (grid, sigma) by hc_build_records: for CSR entry j of cell a with influencer
+ * i, rec4[j] = {cx_i - cx_a, cy_i - cy_a, -0.5*log2(e)/(sigma*size_i)^2,
+ * terrain_i - terrain_a} and rec_dd[j] = depth_i - depth_a (float32). */
+typedef struct {
+    const double *cx, *cy, *size, *terrain, *depth;   /* [n_cells] */
+    const int32_t *tile_index;                         /* [nty][ntx] */
+    int64_t ntx, nty;
+    double xmin, ymin, min_cell;
+    int32_t n_cells;
+    const int32_t *offsets;                            /* [n_cells+1] */
+    const int32_t *indices;                            /* [offsets[n]] */
+    const float *rec4;                                 /* [offsets[n]][4] */
+    const float *rec_dd;                               /* [offsets[n]] */
+    const float *anchor_t, *anchor_d;                  /* [n_cells] terrain/depth of list head, f32 */
+    double sigma;
+} HcGrid;
+
+/* One cascade raster to fill.  cascade.py:395-521 (layout + mask edges),
+ * discretize.py:27-108 (both layers, valid, sentinel). */
+typedef struct {
+    double origin_x, origin_y, texel;
+    int32_t resolution;                  /* R */
+    int32_t n_edges;
+    double edges[HC_MAX_EDGES][5];       /* a_x, a_y, e_x, e_y, -texel*hypot(e) (host) */
+    float *terrain, *water;              /* [R][R] out */
+    uint8_t *valid;                      /* [R][R] out: mask && inside a cell */
+    uint8_t *mask;                       /* [R][R] out, may be NULL */
+} HcCascadeRaster;
+
+/* Max-mip of one (cascade, layer).  raycast.py:40-88 + discretize.py:44-49. */
+typedef struct {
+    const float *heights;                /* [R][R] */
+    const uint8_t *valid;                /* [R][R] */
+    float *mip;                          /* flat levels, level L at level_off[L] */
+    uint8_t *patch_ok;                   /* [(R-1)^2] all four corners valid; may be NULL */
+    int32_t *vrange_key;                 /* [2] ordered-int min/max of valid heights */
+    int32_t resolution;
+    int32_t n_levels;
+    int64_t level_off[HC_MAX_LEVELS];
+    int32_t level_w[HC_MAX_LEVELS];      /* level L is level_w[L] x level_w[L] */
+} HcMipJob;
+
+/* Per-cascade inputs of the fused render kernel (render.py:125-186). */
+typedef struct {
+    double origin_x, origin_y, texel;
+    double rx, ry;                       /* (eye - origin) / texel, host-evaluated */
+    double near_offset, far_offset;      /* polygon offsets along the view axis */
+    int32_t resolution, n_levels;
+    const float *heights[2];             /* terrain, water [R][R] */
+    const uint8_t *valid;                /* [R][R] */
+    const uint8_t *patch_ok;             /* [(R-1)^2], may be NULL */
+    const float *mip[2];                 /* terrain, water */
+    const int32_t *vrange_key;           /* [2 layers][2] ordered-int min/max */
+    int64_t level_off[HC_MAX_LEVELS];
+    int32_t level_w[HC_MAX_LEVELS];
+} HcRenderCascade;
+
+/* Optional per-pixel outputs for parity tests (NULL = not written).  Layer-major:
+ * element [layer * P + pixel]; per-cascade raw records for the near (slot 0)
+ * and blend-partner (slot 1) cascades: [(layer * 2 + slot) * P + pixel]. */
+typedef struct {
+    uint8_t *hit;
+    double *t;
+    int8_t *near_k, *far_k;
+    double *w;
+    double *raw_t;
+    int32_t *raw_ix, *raw_iy;
+    double *raw_u, *raw_v;
+    double *water_depth;                 /* [P]; NaN where the water layer missed */
+    double *dirs;                        /* [P][3] */
+} HcRenderDebug;
+
+typedef struct {
+    int32_t width, height, n_cascades;
+    int32_t x0, y0, x1, y1;              /* pixel sub-rectangle to render (screen tiles) */
+    double eye[3], look[3], right[3], up[3];
+    double tan_half, aspect;             /* host: tan(radians(fov)/2) */
+    double axis_anchor[2], axis_dir[2];  /* ViewAxis of the cascades */
+    double h_lo, h_hi;                   /* grid.height_range */
+    double light[3];                     /* host-normalised _LIGHT_DIR */
+    double cm_lo, cm_hi;                 /* colormap range */
+    double stops[3][3];                  /* colormap stops */
+    uint8_t background[4];
+    HcRenderCascade c[HC_MAX_CASCADES];
+    uint8_t *rgb;                        /* [height][width][3] (full-frame layout) */
+    uint64_t *counters;                  /* HC_CNT_* (RAYS_HIT, NODE_VISITS, PATCH_TESTS), may be NULL */
+    HcRenderDebug dbg;
+} HcRenderArgs;
+
+/* ---- entry points ------------------------------------------------------ */
+
+int hc_abi_version(void);
+const char *hc_last_error(void);
+
+/* Anchored influence records from the CSR table (startup precompute; replaces the
+ * per-batch gather of discretize.py:111-119 + rbf.py:109-123 operand setup). */
+int hc_build_records(const HcGrid *grid, float *rec4, float *rec_dd, float *anchor_t,
+                     float *anchor_d, hc_stream_t stream);
+
+/* Visibility mask only (cascade.py:507-521).  mask is [R][R] uint8. */
+int hc_visibility_mask(const HcCascadeRaster *c, hc_stream_t stream);
+
+/* Frame counters (device uint64[HC_COUNTERS], caller zeroes them per frame). */
+enum {
+    HC_CNT_VISIBLE = 0,      /* masked texels (Frame.visible_texels, render.py:259)   */
+    HC_CNT_VALID = 1,        /* valid texels                                          */
+    HC_CNT_ZERO_WEIGHT = 2,  /* nonzero if some texel had a zero weight sum           */
+    HC_CNT_RAYS_HIT = 3,     /* pixels hit by either layer (Frame.rays_hit)           */
+    HC_CNT_PAIRS = 4,        /* (texel, influencer) pairs evaluated                   */
+    HC_CNT_NODE_VISITS = 5,  /* max-mip node visits (traversal loop iterations)       */
+    HC_CNT_PATCH_TESTS = 6,  /* ray/patch intersection tests                          */
+    HC_COUNTERS = 8
+};
+
+/* Fused mask + cell lookup + Eq. 1/2 for K cascades, both layers
+ * (discretize.py:52-108 for every cascade of a frame in one launch).
+ * Adds to counters VISIBLE, VALID, PAIRS and flags ZERO_WEIGHT (the reference
+ * raises ValueError on a zero weight sum).  counters may be NULL. */
+int hc_discretize(const HcCascadeRaster *cascades, int n_cascades, const HcGrid *grid,
+                  float sentinel, uint64_t *counters, hc_stream_t stream);
+
+/* Max-mips (+ valid ranges + patch validity) for n jobs in two launches
+ * (raycast.py:61-88 and discretize.py:44-49).  `workspace` (device, at least
+ * hc_maxmip_workspace_bytes) holds per-CTA partial min/max; vrange keys are
+ * fully overwritten (no reset needed).  Empty valid set => key(+inf) > key(-inf). */
+size_t hc_maxmip_workspace_bytes(int n_jobs, int max_resolution);
+int hc_maxmip(const HcMipJob *jobs, int n_jobs, void *workspace, size_t workspace_bytes,
+              hc_stream_t stream);
+
+/* Fused camera rays + per-layer traversal over the cascades (early-out
+ * nearest-first, overlap blend) + shading + pixel select
+ * (render.py:100-110,125-186,189-341,249-256). */
+int hc_render(const HcRenderArgs *args, hc_stream_t stream);
+
+/* Drop-in for the reference Numba kernel `_kernels.traverse_batch`
+ * (_kernels.py:218-232): same arguments and per-lane outputs, device pointers,
+ * float32 heights/mip widened to float64 in registers. */
+int hc_traverse_batch(const float *heights, const uint8_t *valid, const float *mflat,
+                      const int64_t *moff, const int64_t *mw, int nlev, int n0,
+                      const double *rx, const double *ry, const double *rz,
+                      const double *dx, const double *dy, const double *dz, int64_t n,
+                      double hmin, double hmax, uint8_t *out_hit, double *out_t,
+                      int32_t *out_ix, int32_t *out_iy, double *out_u, double *out_v,
+                      hc_stream_t stream);
+
+/* Float64 Eq. 2 at arbitrary points (rbf.py:87-156, the `approximate` API):
+ * cells[k] is the containing cell (>= 0).  Outputs terrain, water, wsum, count. */
+int hc_eval_points(const HcGrid *grid, const double *px, const double *py,
+                   const int32_t *cells, int64_t n, double *out_t, double *out_w,
+                   double *out_wsum, int64_t *out_count, hc_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEIGHTCAST_H */

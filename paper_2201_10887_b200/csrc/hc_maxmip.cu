@@ -1,0 +1,237 @@
+// hc_maxmip.cu -- maximum mipmaps, valid height ranges and patch validity.
+//
+// Replaces raycast.py:61-88 (build_max_mipmap: level 0 = max of each bilinear
+// patch's 4 corners, then 2x2 max with -inf padding down to 1x1) and
+// discretize.py:44-49 (CascadeRaster.valid_range: min/max over valid texels,
+// the traversal's height slab).  max/min are exact, so the float32 pyramid
+// equals the reference's pyramid of the same (float32-representable) raster.
+//
+// Two launches for all K cascades x 2 layers of a frame:
+//   k_mip_tiles : one CTA per 32x32 block of level-0 nodes.  The 33x33 height
+//                 tile and its valid bytes are staged in shared memory with
+//                 coalesced loads, then levels 0..5 are reduced in shared
+//                 memory (the block is exactly one level-5 node) and written
+//                 once.  Also emits per-patch validity (the 4-corner test of
+//                 _kernels.py:167-168, terrain job only) and per-CTA partial
+//                 min/max of valid heights.
+//   k_mip_top   : one CTA per job finishes levels 6.. from level 5 (<= 64x64
+//                 nodes at R=2048) and folds the partial min/max into the
+//                 job's valid range.  No atomics, no init pass: deterministic.
+// HBM traffic per job ~ 4*(R^2 + nodes) + R^2 bytes (valid), each byte once.
+#include "hc_internal.cuh"
+
+namespace hc {
+
+constexpr int TILE = 32;            // level-0 nodes per CTA side
+constexpr int TILE_LEVELS = 6;      // levels 0..5 produced per CTA
+
+struct MipParams {
+    HcMipJob j[2 * HC_MAX_CASCADES];
+    float* partial;                 // [n_jobs][max_tiles][2]
+    int32_t max_tiles;
+};
+
+__device__ __forceinline__ int ceil_shift(int n, int s) { return (n + (1 << s) - 1) >> s; }
+
+__global__ void __launch_bounds__(256) k_mip_tiles(const __grid_constant__ MipParams P) {
+    const HcMipJob& J = P.j[blockIdx.z];
+    const int R = J.resolution, n0 = R - 1;
+    const int tiles_x = (n0 + TILE - 1) / TILE;
+    if ((int)blockIdx.x >= tiles_x || (int)blockIdx.y >= tiles_x) return;
+    const int bx = blockIdx.x * TILE, by = blockIdx.y * TILE;
+
+    __shared__ float h[TILE + 1][TILE + 2];
+    __shared__ uint8_t vv[TILE + 1][TILE + 4];
+    __shared__ float lv[TILE][TILE + 1];
+    __shared__ float red[2][8];
+
+    const int tid = threadIdx.x;
+    float vmin = INFINITY, vmax = -INFINITY;
+    // stage the (TILE+1)^2 texel tile; texel (x, y) is "owned" (counted in the
+    // valid range) by the CTA whose node block contains min(x, n0-1)
+    for (int e = tid; e < (TILE + 1) * (TILE + 1); e += 256) {
+        const int ty = e / (TILE + 1), tx = e % (TILE + 1);
+        const int y = by + ty, x = bx + tx;
+        float v = -INFINITY;
+        uint8_t ok = 0;
+        if (x < R && y < R) {
+            const int64_t o = (int64_t)y * R + x;
+            v = J.heights[o];
+            ok = J.valid[o];
+            const bool own_x = tx < TILE || x == R - 1;
+            const bool own_y = ty < TILE || y == R - 1;
+            if (ok && own_x && own_y) {
+                vmin = fminf(vmin, v);
+                vmax = fmaxf(vmax, v);
+            }
+        }
+        h[ty][tx] = v;
+        vv[ty][tx] = ok;
+    }
+    __syncthreads();
+
+    // level 0 (4-corner max) + patch validity
+    for (int e = tid; e < TILE * TILE; e += 256) {
+        const int ty = e / TILE, tx = e % TILE;
+        const int y = by + ty, x = bx + tx;
+        float m = -INFINITY;
+        if (x < n0 && y < n0) {
+            m = fmaxf(fmaxf(h[ty][tx], h[ty][tx + 1]), fmaxf(h[ty + 1][tx], h[ty + 1][tx + 1]));
+            J.mip[(int64_t)y * n0 + x] = m;
+            if (J.patch_ok)
+                J.patch_ok[(int64_t)y * n0 + x] =
+                    vv[ty][tx] & vv[ty][tx + 1] & vv[ty + 1][tx] & vv[ty + 1][tx + 1];
+        }
+        lv[ty][tx] = m;
+    }
+    __syncthreads();
+
+    // levels 1..5 in place: after level L, lv[y][x] for y, x < TILE >> L holds level L
+    for (int L = 1; L < TILE_LEVELS && L < J.n_levels; ++L) {
+        const int side = TILE >> L;
+        const int wl = J.level_w[L];
+        float m = -INFINITY;
+        int y = 0, x = 0;
+        if (tid < side * side) {
+            y = tid / side;
+            x = tid % side;
+            m = fmaxf(fmaxf(lv[2 * y][2 * x], lv[2 * y][2 * x + 1]),
+                      fmaxf(lv[2 * y + 1][2 * x], lv[2 * y + 1][2 * x + 1]));
+        }
+        __syncthreads();
+        if (tid < side * side) {
+            lv[y][x] = m;
+            const int gy = (by >> L) + y, gx = (bx >> L) + x;
+            if (gx < wl && gy < wl) J.mip[J.level_off[L] + (int64_t)gy * wl + gx] = m;
+        }
+        __syncthreads();
+    }
+
+    // CTA partial min/max of valid heights
+    for (int s = 16; s > 0; s >>= 1) {
+        vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, s));
+        vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, s));
+    }
+    if ((tid & 31) == 0) {
+        red[0][tid >> 5] = vmin;
+        red[1][tid >> 5] = vmax;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int w = 1; w < 8; ++w) {
+            vmin = fminf(vmin, red[0][w]);
+            vmax = fmaxf(vmax, red[1][w]);
+        }
+        float* pp = P.partial + ((int64_t)blockIdx.z * P.max_tiles + blockIdx.y * tiles_x + blockIdx.x) * 2;
+        pp[0] = vmin;
+        pp[1] = vmax;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_mip_top(const __grid_constant__ MipParams P) {
+    const HcMipJob& J = P.j[blockIdx.x];
+    const int tid = threadIdx.x;
+    const int tiles_x = (J.resolution - 1 + TILE - 1) / TILE;
+    for (int L = TILE_LEVELS; L < J.n_levels; ++L) {
+        const int w = J.level_w[L], ws = J.level_w[L - 1];
+        const float* src = J.mip + J.level_off[L - 1];
+        float* dst = J.mip + J.level_off[L];
+        for (int e = tid; e < w * w; e += blockDim.x) {
+            const int y = e / w, x = e % w;
+            float v[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int yy = 2 * y + (c >> 1), xx = 2 * x + (c & 1);
+                v[c] = (yy < ws && xx < ws) ? src[(int64_t)yy * ws + xx] : -INFINITY;
+            }
+            dst[(int64_t)y * w + x] = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+        }
+        __syncthreads();
+    }
+    // fold the per-CTA partials (min/max are order independent)
+    __shared__ float red[2][32];
+    float vmin = INFINITY, vmax = -INFINITY;
+    const float* pp = P.partial + (int64_t)blockIdx.x * P.max_tiles * 2;
+    for (int e = tid; e < tiles_x * tiles_x; e += blockDim.x) {
+        vmin = fminf(vmin, pp[2 * e]);
+        vmax = fmaxf(vmax, pp[2 * e + 1]);
+    }
+    for (int s = 16; s > 0; s >>= 1) {
+        vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, s));
+        vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, s));
+    }
+    if ((tid & 31) == 0) {
+        red[0][tid >> 5] = vmin;
+        red[1][tid >> 5] = vmax;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            vmin = fminf(vmin, red[0][w]);
+            vmax = fmaxf(vmax, red[1][w]);
+        }
+        J.vrange_key[0] = float_key(vmin);   // +inf key when no valid texel
+        J.vrange_key[1] = float_key(vmax);
+    }
+}
+
+}  // namespace hc
+
+using namespace hc;
+
+// Shape of the level pyramid; also used by the host to size buffers.
+static int mip_levels(int R, int64_t* off, int32_t* w) {
+    int64_t o = 0;
+    int cw = R - 1, n = 0;
+    for (;;) {
+        if (n >= HC_MAX_LEVELS) return -1;
+        off[n] = o;
+        w[n] = cw;
+        ++n;
+        o += (int64_t)cw * cw;
+        if (cw <= 1) break;
+        cw = (cw + 1) / 2;
+    }
+    return n;
+}
+
+extern "C" size_t hc_maxmip_workspace_bytes(int n_jobs, int max_resolution) {
+    if (n_jobs <= 0 || max_resolution < 2) return 0;
+    const size_t t = (size_t)(max_resolution - 1 + TILE - 1) / TILE;
+    return (size_t)n_jobs * t * t * 2 * sizeof(float);
+}
+
+extern "C" int hc_maxmip(const HcMipJob* jobs, int n_jobs, void* workspace, size_t workspace_bytes,
+                         hc_stream_t stream) {
+    HC_REQUIRE(jobs, "hc_maxmip: null jobs");
+    HC_REQUIRE(n_jobs >= 0 && n_jobs <= 2 * HC_MAX_CASCADES, "hc_maxmip: %d jobs (max %d)", n_jobs,
+               2 * HC_MAX_CASCADES);
+    if (n_jobs == 0) return HC_OK;
+    MipParams P;
+    int tiles_max = 0, rmax = 0;
+    for (int k = 0; k < n_jobs; ++k) {
+        const HcMipJob& J = jobs[k];
+        HC_REQUIRE(J.resolution >= 2, "hc_maxmip: job %d resolution %d < 2", k, J.resolution);
+        HC_REQUIRE(J.heights && J.valid && J.mip && J.vrange_key, "hc_maxmip: job %d null pointer", k);
+        int64_t off[HC_MAX_LEVELS];
+        int32_t w[HC_MAX_LEVELS];
+        const int n = mip_levels(J.resolution, off, w);
+        HC_REQUIRE(n > 0 && n == J.n_levels, "hc_maxmip: job %d has %d levels, expected %d", k, J.n_levels, n);
+        for (int L = 0; L < n; ++L)
+            HC_REQUIRE(off[L] == J.level_off[L] && w[L] == J.level_w[L], "hc_maxmip: job %d level %d shape",
+                       k, L);
+        const int t = (J.resolution - 1 + TILE - 1) / TILE;
+        tiles_max = t > tiles_max ? t : tiles_max;
+        rmax = J.resolution > rmax ? J.resolution : rmax;
+        P.j[k] = J;
+    }
+    const size_t need = hc_maxmip_workspace_bytes(n_jobs, rmax);
+    HC_REQUIRE(workspace && workspace_bytes >= need, "hc_maxmip: workspace %zu bytes < %zu", workspace_bytes,
+               need);
+    P.partial = (float*)workspace;
+    P.max_tiles = tiles_max * tiles_max;
+    dim3 g(tiles_max, tiles_max, n_jobs);
+    k_mip_tiles<<<g, 256, 0, (cudaStream_t)stream>>>(P);
+    k_mip_top<<<n_jobs, 1024, 0, (cudaStream_t)stream>>>(P);
+    return cuda_status("hc_maxmip");
+}

@@ -1,0 +1,225 @@
+"""Per-frame orchestration on the GPU: plan cascades, fill rasters, cast rays, shade.
+
+Drop-in for `heightcast.render` (pkg/src/heightcast/render.py).  `render_frame`
+keeps the reference signature and result type.  Cascade planning is host
+float64 geometry (cascade.py, bit-identical to the reference); everything per
+texel and per pixel runs on the B200 in three launch groups (see _engine.py):
+
+  approximation  hc_discretize            discretize.py:52-108 for all K cascades
+  ray casting    hc_maxmip + hc_render    raycast.py:61-88, render.py:100-341
+
+`Frame.approximation_ms` / `raycast_ms` keep the reference's two phase
+categories (render.py:233-258) but are CUDA-event device times; `plan_ms` is
+the host planning time the reference leaves untimed.  `CascadeSettings.count`
+(default 3, the reference's fixed value) selects K cascades.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _cuda, _engine
+from .cascade import CameraView, NothingVisibleError, plan_cascades
+from .discretize import CascadeRaster
+from .grid import AdaptiveGrid, InfluenceTable
+from .rbf import RbfParams
+
+_COLOR_STOPS = _engine.COLOR_STOPS
+_LIGHT_DIR = _engine.LIGHT_DIR
+
+
+@dataclass(frozen=True)
+class FrameConfig:
+    width: int
+    height: int
+    camera: CameraView
+    colormap_range: tuple[float, float] = (0.0, 5.0)
+    background: tuple[int, int, int] = (30, 40, 60)
+
+    def __post_init__(self):
+        if self.width < 1 or self.height < 1:
+            raise ValueError("image size must be at least 1x1")
+        if not self.colormap_range[0] < self.colormap_range[1]:
+            raise ValueError("colormap range min must be below max")
+
+
+@dataclass(frozen=True)
+class CascadeSettings:
+    resolution: int = 1024
+    overlap: float | str = "auto"
+    count: int = 3
+
+    def __post_init__(self):
+        if not 1 <= self.count <= _cuda.HC_MAX_CASCADES:
+            raise ValueError(f"cascade count must be in 1..{_cuda.HC_MAX_CASCADES}")
+
+
+@dataclass
+class Frame:
+    pixels: np.ndarray                  # (height, width, 3) uint8, row 0 at the top
+    approximation_ms: float
+    raycast_ms: float
+    visible_texels: int = 0
+    rays_hit: int = 0
+    visible: bool = True
+    debug: dict | None = field(default=None, repr=False)
+    plan_ms: float = 0.0
+    valid_texels: int = 0
+
+
+def depth_colormap(depth, colormap_range, background=(0, 0, 0)):
+    """Blue-cyan-white depth gradient (render.py:71-97); host helper for scalar/array use."""
+    lo, hi = colormap_range
+
+    def cmap(d):
+        t = np.clip((d - lo) / (hi - lo), 0.0, 1.0)
+        out = np.empty(t.shape + (3,))
+        for ch in range(3):
+            s0, s1, s2 = _COLOR_STOPS[:, ch]
+            out[..., ch] = np.where(t <= 0.5, s0 + (s1 - s0) * (2.0 * t), s1 + (s2 - s1) * (2.0 * t - 1.0))
+        return np.clip(np.rint(out), 0, 255).astype(np.uint8)
+
+    if isinstance(depth, np.ndarray):
+        rgb = cmap(depth)
+        bad = ~np.isfinite(depth)
+        if bad.any():
+            rgb[bad] = background
+        return rgb
+    if not math.isfinite(depth):
+        return tuple(int(c) for c in background)
+    r = cmap(np.array([float(depth)]))[0]
+    return int(r[0]), int(r[1]), int(r[2])
+
+
+def camera_ray_dirs(camera: CameraView, width: int, height: int) -> np.ndarray:
+    """Per-pixel unit ray directions (render.py:100-110); host helper, the render
+    kernel evaluates the same float64 expression per pixel on the GPU."""
+    right, up, look = camera.basis()
+    th = math.tan(math.radians(camera.fov_y) / 2.0)
+    xs = ((np.arange(width) + 0.5) / width * 2.0 - 1.0) * th * camera.aspect
+    ys = (1.0 - (np.arange(height) + 0.5) / height * 2.0) * th
+    d = look[None, None, :] + xs[None, :, None] * right + ys[:, None, None] * up
+    return d / np.linalg.norm(d, axis=2, keepdims=True)
+
+
+class LayerResolve:
+    """Per-pixel outcome of one layer (render.py:113-122), device tensors.
+
+    `near`/`far` are cascade list indices (-1 = none); `raw[k]` holds
+    (hit, t, ix, iy, u, v) for the pixels whose near or blend cascade is k (the
+    GPU traverses only those; other entries are -1 / 0)."""
+
+    def __init__(self, dbg, layer, K):
+        import torch
+        self.hit = dbg["hit"][layer].bool()
+        self.t = dbg["t"][layer]
+        self.near = dbg["near_k"][layer].to(torch.int32)
+        self.far = dbg["far_k"][layer].to(torch.int32)
+        self.w = dbg["w"][layer]
+        self.raw_slots = {name: dbg["raw_" + name][layer] for name in ("t", "ix", "iy", "u", "v")}
+        self.raw = {}
+        for k in range(K):
+            sel0 = self.hit & (self.near == k)
+            sel1 = self.hit & (self.far == k)
+            vals = []
+            for name, fill in (("t", 0.0), ("ix", -1), ("iy", -1), ("u", 0.0), ("v", 0.0)):
+                s = self.raw_slots[name]
+                base = torch.full_like(s[0], fill)
+                base = torch.where(sel0, s[0], base)
+                vals.append(torch.where(sel1, s[1], base))
+            self.raw[k] = (sel0 | sel1, *vals)
+
+
+_BUFFERS: dict = {}
+
+
+def _frame_buffers(device, K, R, W, H, debug):
+    import torch
+    key = (str(device), K, R, W, H, bool(debug))
+    buf = _BUFFERS.get(key)
+    if buf is None:
+        if len(_BUFFERS) > 8:
+            _BUFFERS.clear()
+        buf = _engine.FrameBuffers(torch.device(device), K, R, W, H, debug=debug)
+        _BUFFERS[key] = buf
+    return buf
+
+
+def _background_frame(config, debug):
+    px = np.empty((config.height, config.width, 3), dtype=np.uint8)
+    px[:] = np.asarray(config.background, dtype=np.uint8)
+    return Frame(px, 0.0, 0.0, 0, 0, visible=False, debug={"visible": False} if debug else None)
+
+
+def render_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable, params: RbfParams,
+                 settings: CascadeSettings = CascadeSettings(), debug: bool = False) -> Frame:
+    """Render one frame on the GPU; same inputs/outputs as the reference."""
+    import torch
+    if table.sigma != params.sigma:
+        raise ValueError("influence table was built for a different sigma")
+    _cuda.require_cuda()
+    tp = time.perf_counter()
+    try:
+        hull, polygons, layouts = plan_cascades(config.camera, grid, settings.resolution,
+                                                settings.overlap, settings.count)
+    except NothingVisibleError:
+        return _background_frame(config, debug)
+    plan_ms = (time.perf_counter() - tp) * 1e3
+    active = [lay for lay in layouts if lay is not None]
+    gdev = grid.device_view()
+    ginf = gdev.influence(table)
+    buf = _frame_buffers(gdev.device, len(active), settings.resolution, config.width,
+                         config.height, debug)
+    fd = _engine.pack_frame(buf, active, config.camera, grid, config.width, config.height,
+                            config.colormap_range, config.background)
+    with torch.cuda.device(gdev.device):
+        _engine.launch_frame(buf, fd, ginf, grid.height_range[0] - 1.0)
+        pixels = torch.empty((config.height, config.width, 3), dtype=torch.uint8, pin_memory=True)
+        pixels.copy_(buf.rgb, non_blocking=True)
+        buf.counters_host.copy_(buf.counters, non_blocking=True)
+        buf.ev[3].record()
+        buf.ev[3].synchronize()
+    cnt = buf.counters_host.tolist()
+    if cnt[_cuda.CNT_ZERO_WEIGHT]:
+        raise ValueError(f"zero weight sum while discretizing: influence table inconsistent "
+                         f"with sigma={params.sigma}")
+    frame = Frame(pixels.numpy(), buf.ev[0].elapsed_time(buf.ev[1]), buf.ev[1].elapsed_time(buf.ev[2]),
+                  visible_texels=int(cnt[_cuda.CNT_VISIBLE]), rays_hit=int(cnt[_cuda.CNT_RAYS_HIT]),
+                  plan_ms=plan_ms, valid_texels=int(cnt[_cuda.CNT_VALID]))
+    frame.work = {"pairs": int(cnt[_cuda.CNT_PAIRS]), "node_visits": int(cnt[_cuda.CNT_NODE_VISITS]),
+                  "patch_tests": int(cnt[_cuda.CNT_PATCH_TESTS])}
+    if debug:
+        for k, lay in enumerate(active):
+            lay.mask = buf.mask[k].clone().bool()
+        rasters = [CascadeRaster(lay, buf.terrain[k].clone(), buf.water[k].clone(),
+                                 buf.valid[k].bool(), grid.height_range[0] - 1.0)
+                   for k, lay in enumerate(active)]
+        rasters += [None] * (len(layouts) - len(active))
+        d = buf.dbg
+        frame.debug = {"visible": True, "layouts": layouts, "rasters": rasters,
+                       "terrain": LayerResolve(d, 0, len(active)),
+                       "water": LayerResolve(d, 1, len(active)),
+                       "dirs": d["dirs"].clone(), "water_depth": d["water_depth"].clone(),
+                       "polygons": polygons, "hull": hull,
+                       "mips": {"terrain": [buf.mip[k, 0].clone() for k in range(len(active))],
+                                "water": [buf.mip[k, 1].clone() for k in range(len(active))]},
+                       "vrange_keys": buf.vrange.clone()}
+    return frame
+
+
+def write_ppm(pixels, target) -> None:
+    """Binary PPM (P6, maxval 255) of an (H, W, 3) uint8 image (render.py:344-354)."""
+    arr = pixels.detach().cpu().numpy() if hasattr(pixels, "detach") else np.asarray(pixels)
+    h, w = arr.shape[:2]
+    header = f"P6\n{w} {h}\n255\n".encode("ascii")
+    if hasattr(target, "write"):
+        target.write(header)
+        target.write(arr.astype(np.uint8).tobytes())
+    else:
+        with open(target, "wb") as fh:
+            fh.write(header)
+            fh.write(arr.astype(np.uint8).tobytes())
