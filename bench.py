@@ -1,0 +1,373 @@
+"""Benchmark: frames/s of the B200 heightcast hot path (BASELINE.json metric), one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A step renders one full frame of the configuration (C2 by default: 100k-cell
+adaptive quadtree, 4 cascades of 1024^2, 1920x1080) -- host cascade planning,
+GPU mask + RBF discretization, max mipmaps, ray casting and shading.
+`value`  : frames/s with the grid resident in HBM, each step timed with CUDA
+           events on the launching stream (host planning included, since the GPU
+           waits for it), L2 flushed (256 MiB write) between timed steps.
+`e2e`    : frames/s through the public API `render_frame(...)` (host-planned,
+           kernel descriptors copied host->device as launch parameters, pixels
+           read back into pinned host memory), host wall clock per call.
+`roofline`: the dominant kernel's algorithmic work per launch / its mean event
+           duration vs MEASURED_PEAKS.json (see DESIGN.md for the unit models).
+`cpu_baseline`: the float64 C oracle port of the reference pipeline
+           (oracle/, OpenMP over all host cores) on rank 0, bounded sample.
+N>1: one process per GPU (torchrun), each rank renders its own camera view of
+the same grid (view sharding, no data-path collective): weak scaling; the
+reported value is total frames/s, timed as the max over ranks.
+`--impl reference`: times the oracle port of the reference's CPU pipeline on
+the host cores (rank 0 only) for the same config/metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+B200_SMS = 148
+MUFU_PER_SM_CLK = 16          # ex2 lanes per SM per clock (SURVEY.md §8 d)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="cpu_baseline sample budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_PATH) as fh:
+            p = json.load(fh)
+        return p, "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v.strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def build_inputs(cfg):
+    from paper_2201_10887_b200 import build_influence_table
+    t0 = time.perf_counter()
+    g = cfg.grid()
+    t1 = time.perf_counter()
+    table = build_influence_table(g, cfg.sigma)
+    t2 = time.perf_counter()
+    return g, table, {"synth_s": round(t1 - t0, 2), "influence_table_s": round(t2 - t1, 2)}
+
+
+def rank_frame_config(cfg, rank, world):
+    """Rank r renders view r: the config camera rotated about the domain centre."""
+    if world == 1 or cfg.views > 1:
+        return cfg.frame_config(rank % max(cfg.views, 1))
+    from paper_2201_10887_b200.cascade import CameraView
+    from paper_2201_10887_b200.render import FrameConfig
+    c = cfg.camera(0)
+    ang = 2.0 * math.pi * rank / world
+    cx, cy = 1024.0, 1024.0
+    ca, sa = math.cos(ang), math.sin(ang)
+    rot = lambda p: (cx + ca * (p[0] - cx) - sa * (p[1] - cy), cy + sa * (p[0] - cx) + ca * (p[1] - cy), p[2])
+    eye, la = rot(cfg.eye), rot(cfg.look_at)
+    cam = CameraView(eye=eye, look_dir=tuple(b - a for a, b in zip(eye, la)), up=c.up, fov_y=c.fov_y,
+                     aspect=c.aspect, near_clip=c.near_clip, far_clip=c.far_clip)
+    return FrameConfig(width=cfg.width, height=cfg.height, camera=cam)
+
+
+def cpu_frames(cfg, g, table, fc, budget_s, max_frames=None):
+    """Oracle (reference CPU port) frames: returns (frames/s, per-frame stats, n)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import heightcast_oracle as O
+    from paper_2201_10887_b200.rbf import RbfParams
+    O.build()
+    P = RbfParams(sigma=cfg.sigma)
+    st = cfg.settings()
+    O.render_frame(fc, g, table, P, st)              # warm (page-in, thread pool)
+    times, stats = [], None
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        _, stats = O.render_frame(fc, g, table, P, st)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start >= budget_s or (max_frames and len(times) >= max_frames):
+            break
+    per = statistics.median(times)
+    return 1.0 / per, stats, len(times), per
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    g, table, _ = build_inputs(cfg)
+    fc = rank_frame_config(cfg, 0, 1)
+    fps, stats, n, per = cpu_frames(cfg, g, table, fc, budget_s=1e9, max_frames=args.steps)
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    line = {
+        "impl": "reference", "metric": "frames/sec", "value": fps, "unit": "frames/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.description}", "grid_cells": g.n_cells, "cascades": cfg.cascades,
+                   "cascade_res": cfg.resolution, "image": [cfg.width, cfg.height], "sigma": cfg.sigma},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "port",
+                         "sample": f"{n} full {cfg.name} frames (float64 C oracle of the reference pipeline, "
+                                   f"OpenMP {cores} threads), median"},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "phases_ms": {k: round(stats[k], 3) for k in ("plan_ms", "approximation_ms", "raycast_ms")},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    from paper_2201_10887_b200.configs import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    from paper_2201_10887_b200 import render_frame
+    from paper_2201_10887_b200 import _cuda, _engine
+    from paper_2201_10887_b200.render import enqueue_frame
+    from paper_2201_10887_b200.rbf import RbfParams
+
+    g, table, prep = build_inputs(cfg)
+    fc = rank_frame_config(cfg, rank, ws)
+    st = cfg.settings()
+    P = RbfParams(sigma=cfg.sigma)
+    t_up = time.perf_counter()
+    gdev = g.device_view(dev)
+    gdev.influence(table)
+    torch.cuda.synchronize()
+    prep["upload_s"] = round(time.perf_counter() - t_up, 3)
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warm-up (device-resident path)
+    for _ in range(max(args.warmup, 3)):
+        enqueue_frame(fc, g, table, st)
+    torch.cuda.synchronize()
+
+    # ---- timed: K steps, each bracketed by CUDA events, L2 flushed between steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    k_disc, k_mip, k_ren = [], [], []
+    barrier()
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            ev[i][0].record()
+            buf, plan = enqueue_frame(fc, g, table, st)
+            ev[i][1].record()
+            ev[i][1].synchronize()
+            k_disc.append(buf.ev[0].elapsed_time(buf.ev[1]))
+            k_mip.append(buf.ev[1].elapsed_time(buf.ev[4]))
+            k_ren.append(buf.ev[4].elapsed_time(buf.ev[2]))
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    if ws > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = ws * args.steps / (total_ms / 1e3)
+
+    cnt = buf.counters.cpu().tolist()
+    work = {"pairs": cnt[_cuda.CNT_PAIRS], "node_visits": cnt[_cuda.CNT_NODE_VISITS],
+            "patch_tests": cnt[_cuda.CNT_PATCH_TESTS], "valid_texels": cnt[_cuda.CNT_VALID],
+            "visible_texels": cnt[_cuda.CNT_VISIBLE], "rays_hit": cnt[_cuda.CNT_RAYS_HIT]}
+
+    # ---- e2e through the public API (pixels to pinned host memory every step)
+    for _ in range(2):
+        render_frame(fc, g, table, P, st)
+    barrier()
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fr = render_frame(fc, g, table, P, st)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    barrier()
+    e2e_total = sum(e2e_ms)
+    if ws > 1:
+        t = torch.tensor([e2e_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = ws * args.steps / (e2e_total / 1e3)
+
+    # ---- rooflines (algorithmic work per launch / mean launch time)
+    peaks, peak_kind = load_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    mufu_peak = B200_SMS * MUFU_PER_SM_CLK * sm_max * 1e6          # ex2/s = pairs/s bound
+    hbm = float(peaks["hbm_gbs"])
+    K = len(plan[3])
+    R = cfg.resolution
+    _, _, nodes = _engine.mip_shape(R)
+    mip_bytes = 2 * K * (4 * (R * R + nodes) + R * R)
+    trav_bytes = 4 * work["node_visits"] + 20 * work["patch_tests"] + 3 * cfg.width * cfg.height
+    mean = lambda xs: sum(xs) / len(xs)
+    kernels = {
+        "hc_discretize": {"ms": mean(k_disc), "bound": "sfu", "unit": "Gpairs/s",
+                          "achieved": work["pairs"] / (mean(k_disc) * 1e-3) / 1e9,
+                          "peak": mufu_peak / 1e9, "work_per_launch": work["pairs"],
+                          "work_model": "(valid texel, influence-list entry) pairs; 1 ex2 each"},
+        "hc_maxmip": {"ms": mean(k_mip), "bound": "hbm", "unit": "GB/s",
+                      "achieved": mip_bytes / (mean(k_mip) * 1e-3) / 1e9, "peak": hbm,
+                      "work_per_launch": mip_bytes, "work_model": "2K x (4(R^2+nodes)+R^2) bytes"},
+        "hc_render": {"ms": mean(k_ren), "bound": "hbm", "unit": "GB/s",
+                      "achieved": trav_bytes / (mean(k_ren) * 1e-3) / 1e9, "peak": hbm,
+                      "work_per_launch": trav_bytes,
+                      "work_model": "4 B x node visits + 20 B x patch tests + 3 B x pixels"},
+    }
+    for k in kernels.values():
+        k["frac"] = k["achieved"] / k["peak"]
+    dominant = max(kernels, key=lambda n: kernels[n]["ms"])
+    traffic = None
+    try:
+        with open(PROFILE_SUMMARY) as fh:
+            traffic = json.load(fh).get(cfg.name, {}).get(dominant)
+    except (OSError, ValueError):
+        pass
+    d = kernels[dominant]
+    roofline = {"kernel": dominant, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
+                "unit": d["unit"], "frac": d["frac"], "traffic": traffic,
+                "peak_source": f"{peak_kind} MEASURED_PEAKS.json" if d["bound"] == "hbm"
+                else f"148 SMs x 16 ex2/clk x {sm_max:.0f} MHz ({peak_kind} sm_max_mhz)"}
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if ws == 1 and not args.no_cpu_baseline:
+            fps, stats, n, per = cpu_frames(cfg, g, table, fc, budget_s=args.cpu_seconds)
+            cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+            cpu = {"value": fps, "unit": "frames/s", "cores": cores, "kind": "port",
+                   "sample": f"{n} full {cfg.name} frames (float64 C oracle of the reference pipeline, "
+                             f"OpenMP {cores} threads, ~{args.cpu_seconds:.0f} s budget), median",
+                   "phases_ms": {k: round(stats[k], 3) for k in ("plan_ms", "approximation_ms", "raycast_ms")}}
+        P_pix = cfg.width * cfg.height
+        out = {
+            "metric": "frames/sec", "value": value, "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64 traversal/shading, f32 RBF discretization", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {cfg.description}", "grid_cells": g.n_cells,
+                       "mean_influence_list": round(len(table.indices) / g.n_cells, 2), "sigma": cfg.sigma,
+                       "cascades": K, "cascade_res": R, "image": [cfg.width, cfg.height],
+                       "l2": "256 MiB flush between timed steps", "parallelism": f"view-sharded x{ws}"},
+            "rays_per_sec": value * P_pix, "layer_rays_per_sec": value * 2 * P_pix,
+            "texels_per_sec": value * work["valid_texels"] / ws,
+            "e2e": {"value": e2e_value, "unit": "frames/s",
+                    "h2d_bytes_per_step": _frame_param_bytes(K),
+                    "d2h_bytes_per_step": P_pix * 3 + 8 * _cuda.N_COUNTERS,
+                    "ms_per_step": e2e_total / args.steps},
+            "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu,
+            "clocks": clocks.summary(), "gpu_launches": _engine.LAUNCHES_PER_FRAME * args.steps,
+            "work_per_frame": work,
+            "phases_ms": {"plan_ms": round(plan[4], 3), "approximation_ms": round(mean(k_disc), 4),
+                          "raycast_ms": round(mean(k_mip) + mean(k_ren), 4)},
+            "prep": prep,
+        }
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _frame_param_bytes(K):
+    import ctypes as C
+    from paper_2201_10887_b200 import _cuda
+    return (C.sizeof(_cuda.HcCascadeRaster) * K + C.sizeof(_cuda.HcMipJob) * 2 * K
+            + C.sizeof(_cuda.HcRenderArgs))
+
+
+if __name__ == "__main__":
+    main()

@@ -105,7 +105,8 @@ class FrameBuffers:
         self.dbg = None
         if debug:
             self.alloc_debug()
-        self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        # events: 0 frame start, 1 after discretize, 2 after render, 3 read-back done, 4 after maxmip
+        self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
 
     def alloc_debug(self):
         import torch
@@ -198,6 +199,9 @@ def pack_frame(buf: FrameBuffers, layouts, camera, grid, width, height, colormap
     return FrameDescriptors(rasters, jobs, A, K)
 
 
+LAUNCHES_PER_FRAME = 4   # hc_discretize (1) + hc_maxmip (2) + hc_render (1)
+
+
 def launch_frame(buf: FrameBuffers, fd: FrameDescriptors, ginf, sentinel: float, stream=None,
                  timing: bool = True):
     """Enqueue discretize -> maxmip -> render on `stream` (no host sync)."""
@@ -214,6 +218,8 @@ def launch_frame(buf: FrameBuffers, fd: FrameDescriptors, ginf, sentinel: float,
     if fd.K:
         _cuda.check(L.hc_maxmip(fd.jobs, 2 * fd.K, buf.mip_ws.data_ptr(), buf.mip_ws.numel(), s),
                     "hc_maxmip")
+    if timing:
+        buf.ev[4].record()
     _cuda.check(L.hc_render(C.byref(fd.render), s), "hc_render")
     if timing:
         buf.ev[2].record()

@@ -155,19 +155,19 @@ def _background_frame(config, debug):
     return Frame(px, 0.0, 0.0, 0, 0, visible=False, debug={"visible": False} if debug else None)
 
 
-def render_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable, params: RbfParams,
-                 settings: CascadeSettings = CascadeSettings(), debug: bool = False) -> Frame:
-    """Render one frame on the GPU; same inputs/outputs as the reference."""
-    import torch
-    if table.sigma != params.sigma:
-        raise ValueError("influence table was built for a different sigma")
-    _cuda.require_cuda()
+def enqueue_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable,
+                  settings: CascadeSettings = CascadeSettings(), debug: bool = False, rect=None):
+    """Plan on the host and enqueue one frame's kernels on the current stream.
+
+    Returns (buffers, plan) without waiting for the GPU, or None when nothing is
+    visible.  The device-resident half of `render_frame`; pixels stay in
+    `buffers.rgb` until read back."""
     tp = time.perf_counter()
     try:
         hull, polygons, layouts = plan_cascades(config.camera, grid, settings.resolution,
                                                 settings.overlap, settings.count)
     except NothingVisibleError:
-        return _background_frame(config, debug)
+        return None
     plan_ms = (time.perf_counter() - tp) * 1e3
     active = [lay for lay in layouts if lay is not None]
     gdev = grid.device_view()
@@ -175,9 +175,24 @@ def render_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable,
     buf = _frame_buffers(gdev.device, len(active), settings.resolution, config.width,
                          config.height, debug)
     fd = _engine.pack_frame(buf, active, config.camera, grid, config.width, config.height,
-                            config.colormap_range, config.background)
-    with torch.cuda.device(gdev.device):
-        _engine.launch_frame(buf, fd, ginf, grid.height_range[0] - 1.0)
+                            config.colormap_range, config.background, rect=rect)
+    _engine.launch_frame(buf, fd, ginf, grid.height_range[0] - 1.0)
+    return buf, (hull, polygons, layouts, active, plan_ms)
+
+
+def render_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable, params: RbfParams,
+                 settings: CascadeSettings = CascadeSettings(), debug: bool = False) -> Frame:
+    """Render one frame on the GPU; same inputs/outputs as the reference."""
+    import torch
+    if table.sigma != params.sigma:
+        raise ValueError("influence table was built for a different sigma")
+    _cuda.require_cuda()
+    dev = grid.device_view().device
+    with torch.cuda.device(dev):
+        queued = enqueue_frame(config, grid, table, settings, debug)
+        if queued is None:
+            return _background_frame(config, debug)
+        buf, (hull, polygons, layouts, active, plan_ms) = queued
         pixels = torch.empty((config.height, config.width, 3), dtype=torch.uint8, pin_memory=True)
         pixels.copy_(buf.rgb, non_blocking=True)
         buf.counters_host.copy_(buf.counters, non_blocking=True)
