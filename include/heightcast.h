@@ -139,6 +139,13 @@ typedef struct {
     HcRenderCascade c[HC_MAX_CASCADES];
     uint8_t *rgb;                        /* [height][width][3] (full-frame layout) */
     uint64_t *counters;                  /* HC_CNT_* (RAYS_HIT, NODE_VISITS, PATCH_TESTS), may be NULL */
+    /* persistent-warp tile queue over 4x4-pixel tiles of [x0,x1) x [y0,y1)
+     * (hc_render_tiles of them): */
+    uint32_t *tile_counter;              /* queue head (device, 1 word), reset by hc_render   */
+    int32_t *tile_cost;                  /* [tiles] in: previous launch's costs, out: this one's
+                                          * (max node visits of a lane in the tile); may be NULL */
+    int32_t *tile_order;                 /* [tiles] scratch for the heaviest-first order; NULL =
+                                          * raster order (requires tile_cost when set) */
     HcRenderDebug dbg;
 } HcRenderArgs;
 
@@ -187,6 +194,9 @@ int hc_maxmip(const HcMipJob *jobs, int n_jobs, void *workspace, size_t workspac
  * (render.py:100-110,125-186,189-341,249-256). */
 int hc_render(const HcRenderArgs *args, hc_stream_t stream);
 
+/* Number of 4x4-pixel tiles hc_render schedules for a pixel rectangle. */
+size_t hc_render_tiles(int x0, int y0, int x1, int y1);
+
 /* Drop-in for the reference Numba kernel `_kernels.traverse_batch`
  * (_kernels.py:218-232): same arguments and per-lane outputs, device pointers,
  * float32 heights/mip widened to float64 in registers. */
@@ -203,6 +213,10 @@ int hc_traverse_batch(const float *heights, const uint8_t *valid, const float *m
 int hc_eval_points(const HcGrid *grid, const double *px, const double *py,
                    const int32_t *cells, int64_t n, double *out_t, double *out_w,
                    double *out_wsum, int64_t *out_count, hc_stream_t stream);
+
+/* Self-test of the hoisted float64 division used by the traversal: counts operand
+ * pairs (n pseudo-random + structured) where it differs from IEEE a / b. */
+int hc_selftest_division(uint64_t n, uint64_t seed, uint64_t *mismatches, hc_stream_t stream);
 
 #ifdef __cplusplus
 }

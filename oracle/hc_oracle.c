@@ -255,7 +255,7 @@ static int patch_roots(double h00, double h10, double h01, double h11, double u0
 static hco_hit traverse_one(const double *H, const uint8_t *V, const double *mflat,
                             const int64_t *moff, const int64_t *mw, int nlev, int64_t n0,
                             double rx, double ry, double rz, double dx, double dy, double dz,
-                            double hmin, double hmax)
+                            double hmin, double hmax, int32_t *visits)
 {
     const hco_hit miss = {0, 0.0, -1, -1, 0.0, 0.0};
     const int64_t R = n0 + 1;
@@ -284,6 +284,7 @@ static hco_hit traverse_one(const double *H, const uint8_t *V, const double *mfl
     double t = t0;
     int level = nlev - 1;
     for (;;) {
+        if (visits) *visits += 1;
         const int64_t nx = cx >> level, ny = cy >> level;
         const double x0 = (double)(nx << level), y0 = (double)(ny << level);
         const double x1 = x0 + (double)((int64_t)1 << level), y1 = y0 + (double)((int64_t)1 << level);
@@ -339,12 +340,15 @@ void hco_traverse_batch(const double *heights, const uint8_t *valid, const doubl
                         const double *rx, const double *ry, const double *rz,
                         const double *dx, const double *dy, const double *dz, int64_t n,
                         double hmin, double hmax, uint8_t *out_hit, double *out_t,
-                        int32_t *out_ix, int32_t *out_iy, double *out_u, double *out_v)
+                        int32_t *out_ix, int32_t *out_iy, double *out_u, double *out_v,
+                        int32_t *out_visits /* may be NULL: node visits per ray */)
 {
 #pragma omp parallel for schedule(dynamic, 512)
     for (int64_t i = 0; i < n; ++i) {
+        if (out_visits) out_visits[i] = 0;
         const hco_hit h = traverse_one(heights, valid, mflat, moff, mw, nlev, n0, rx[i], ry[i],
-                                       rz[i], dx[i], dy[i], dz[i], hmin, hmax);
+                                       rz[i], dx[i], dy[i], dz[i], hmin, hmax,
+                                       out_visits ? out_visits + i : 0);
         out_hit[i] = (uint8_t)h.hit;
         out_t[i] = h.t;
         out_ix[i] = h.ix;

@@ -14,7 +14,7 @@ import subprocess
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(PKG_DIR, "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "libheightcast_cuda.so")
+LIB_PATH = os.environ.get("HC_LIB_PATH") or os.path.join(LIB_DIR, "libheightcast_cuda.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 
 HC_ABI_VERSION = 1
@@ -28,8 +28,8 @@ N_COUNTERS = 8
 
 # exported symbols, in header order (tests check the .so exports all of them)
 EXPORTS = ("hc_abi_version", "hc_last_error", "hc_build_records", "hc_visibility_mask",
-           "hc_discretize", "hc_maxmip_workspace_bytes", "hc_maxmip", "hc_render",
-           "hc_traverse_batch", "hc_eval_points")
+           "hc_discretize", "hc_maxmip_workspace_bytes", "hc_maxmip", "hc_render", "hc_render_tiles",
+           "hc_traverse_batch", "hc_eval_points", "hc_selftest_division")
 
 _vp = C.c_void_p
 _d = C.c_double
@@ -77,7 +77,7 @@ class HcRenderArgs(C.Structure):
                 ("axis_dir", _d * 2), ("h_lo", _d), ("h_hi", _d), ("light", _d * 3),
                 ("cm_lo", _d), ("cm_hi", _d), ("stops", _d * 9), ("background", C.c_uint8 * 4),
                 ("c", HcRenderCascade * HC_MAX_CASCADES), ("rgb", _vp), ("counters", _vp),
-                ("dbg", HcRenderDebug)]
+                ("tile_counter", _vp), ("tile_cost", _vp), ("tile_order", _vp), ("dbg", HcRenderDebug)]
 
 
 class HeightcastCudaError(RuntimeError):
@@ -116,6 +116,9 @@ def lib():
     L.hc_render.argtypes = [C.POINTER(HcRenderArgs), _vp]
     L.hc_traverse_batch.argtypes = [_vp, _vp, _vp, _vp, _vp, C.c_int, C.c_int] + [_vp] * 6 + \
         [_i64, _d, _d] + [_vp] * 6 + [_vp]
+    L.hc_render_tiles.restype = C.c_size_t
+    L.hc_render_tiles.argtypes = [C.c_int] * 4
+    L.hc_selftest_division.argtypes = [C.c_uint64, C.c_uint64, _vp, _vp]
     L.hc_eval_points.argtypes = [C.POINTER(HcGrid), _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
     ver = L.hc_abi_version()
     if ver != HC_ABI_VERSION:

@@ -100,6 +100,10 @@ class FrameBuffers:
         # node visits, patch tests
         self.counters = torch.zeros(_cuda.N_COUNTERS, dtype=torch.int64, device=dev)
         self.rgb = torch.empty((H, W, 3), dtype=torch.uint8, device=dev)
+        n_tiles = _cuda.lib().hc_render_tiles(0, 0, W, H)
+        self.tile_cost = torch.zeros(max(n_tiles, 1), dtype=torch.int32, device=dev)
+        self.tile_order = torch.empty(max(n_tiles, 1), dtype=torch.int32, device=dev)
+        self.tile_counter = torch.zeros(1, dtype=torch.int32, device=dev)
         self.rgb_host = torch.empty((H, W, 3), dtype=torch.uint8, pin_memory=True)
         self.counters_host = torch.empty(_cuda.N_COUNTERS, dtype=torch.int64, pin_memory=True)
         self.dbg = None
@@ -193,13 +197,17 @@ def pack_frame(buf: FrameBuffers, layouts, camera, grid, width, height, colormap
             c.level_w[L] = w[L]
     A.rgb = buf.rgb.data_ptr()
     A.counters = buf.counters.data_ptr()
+    A.tile_counter = buf.tile_counter.data_ptr()
+    if rect is None:       # costs/order are per full-frame tile grid
+        A.tile_cost = buf.tile_cost.data_ptr()
+        A.tile_order = buf.tile_order.data_ptr()
     if buf.dbg is not None:
         for name, t in buf.dbg.items():
             setattr(A.dbg, name, t.data_ptr())
     return FrameDescriptors(rasters, jobs, A, K)
 
 
-LAUNCHES_PER_FRAME = 4   # hc_discretize (1) + hc_maxmip (2) + hc_render (1)
+LAUNCHES_PER_FRAME = 5   # hc_discretize (1) + hc_maxmip (2) + hc_render (2: tile order, render)
 
 
 def launch_frame(buf: FrameBuffers, fd: FrameDescriptors, ginf, sentinel: float, stream=None,
