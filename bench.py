@@ -245,7 +245,7 @@ def main():
             flush.zero_()
             torch.cuda.synchronize()
             ev[i][0].record()
-            buf, plan = enqueue_frame(fc, g, table, st)
+            buf, plan, plan_ms = enqueue_frame(fc, g, table, st)
             ev[i][1].record()
             ev[i][1].synchronize()
             k_disc.append(buf.ev[0].elapsed_time(buf.ev[1]))
@@ -290,7 +290,7 @@ def main():
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     mufu_peak = B200_SMS * MUFU_PER_SM_CLK * sm_max * 1e6          # ex2/s = pairs/s bound
     hbm = float(peaks["hbm_gbs"])
-    K = len(plan[3])
+    K = plan.n_active
     R = cfg.resolution
     _, _, nodes = _engine.mip_shape(R)
     mip_bytes = 2 * K * (4 * (R * R + nodes) + R * R)
@@ -352,7 +352,7 @@ def main():
             "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu,
             "clocks": clocks.summary(), "gpu_launches": _engine.LAUNCHES_PER_FRAME * args.steps,
             "work_per_frame": work,
-            "phases_ms": {"plan_ms": round(plan[4], 3), "approximation_ms": round(mean(k_disc), 4),
+            "phases_ms": {"plan_ms": round(plan_ms, 4), "approximation_ms": round(mean(k_disc), 4),
                           "raycast_ms": round(mean(k_mip) + mean(k_ren), 4)},
             "prep": prep,
         }

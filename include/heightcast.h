@@ -149,6 +149,63 @@ typedef struct {
     HcRenderDebug dbg;
 } HcRenderArgs;
 
+/* ---- host cascade planning (cascade.py:38-562), float64, bit-identical ---- */
+
+#define HC_MAX_HULL 64
+
+typedef struct {
+    double eye[3], look[3], up[3];       /* look/up unit vectors (CameraView.__post_init__) */
+    double fov_y, aspect, near_clip, far_clip;
+} HcCamera;
+
+typedef struct {
+    double xmin, ymin, xmax, ymax;       /* grid.domain */
+    double h_lo, h_hi;                   /* grid.height_range */
+    double min_cell;
+} HcDomain;
+
+typedef struct {
+    int32_t present;                     /* 0: degenerate cascade (None in the reference) */
+    int32_t n_verts;
+    double verts[HC_MAX_EDGES][2];       /* CCW polygon */
+    double near_offset, far_offset;
+    double origin[2], texel;             /* texel (ix, iy) centre = origin + (ix, iy) * texel */
+    int32_t resolution;
+    int32_t box_texel[2], box_steps[2];
+    double edges[HC_MAX_EDGES][5];       /* mask edge table, thr = -texel * math.hypot(e) */
+} HcCascadePlan;
+
+typedef struct {
+    int32_t status;                      /* 0 ok, 1 frustum misses the volume, 2 degenerate area */
+    int32_t n_hull;
+    double hull[HC_MAX_HULL][2];
+    double overlap;                      /* resolved overlap (metres) */
+    double axis_anchor[2], axis_dir[2];  /* ViewAxis shared by all cascades */
+    int32_t count, n_active;
+    HcCascadePlan c[HC_MAX_CASCADES];
+} HcPlan;
+
+/* r = q^(1/count) for the logarithmic splits; the reference evaluates it with
+ * numpy (np.cbrt for 3 cascades), whose SIMD implementation can differ from libm
+ * in the last bit, so Python callers pass numpy's; NULL = libm cbrt/sqrt/pow. */
+typedef double (*hc_root_fn)(double q, int count);
+
+/* CPython 3.12 math.hypot(a, b) (the reference evaluates mask thresholds with it). */
+double hc_py_hypot(double a, double b);
+/* visible_hull (cascade.py:150-202).  *n_out = vertex count, or -1 (frustum misses
+ * the volume) / -2 (degenerate area) -- NothingVisibleError in the reference. */
+int hc_visible_hull(const HcCamera *cam, const HcDomain *dom, double *hull_xy, int capacity, int *n_out);
+/* clip_cascade_polygons (cascade.py:310-388), generalised to `count` cascades
+ * (count == 3 is the reference).  Fills polygons and offsets of out->c[0..count). */
+int hc_clip_cascades(const double *hull_xy, int n_hull, const double *view_dir, double overlap,
+                     const double *eye_xy, int count, hc_root_fn root, HcPlan *out);
+/* fit_layout (cascade.py:438-504) incl. the mask edge table; min_texel < 0 = None. */
+int hc_fit_layout(const double *verts_xy, int n, int resolution, double min_cell, double min_texel,
+                  HcCascadePlan *out);
+/* plan_cascades (cascade.py:539-562) for `count` cascades; overlap < 0 means "auto". */
+int hc_plan_cascades(const HcCamera *cam, const HcDomain *dom, int resolution, double overlap, int count,
+                     hc_root_fn root, HcPlan *out);
+
 /* ---- entry points ------------------------------------------------------ */
 
 int hc_abi_version(void);
@@ -213,6 +270,37 @@ int hc_traverse_batch(const float *heights, const uint8_t *valid, const float *m
 int hc_eval_points(const HcGrid *grid, const double *px, const double *py,
                    const int32_t *cells, int64_t n, double *out_t, double *out_w,
                    double *out_wsum, int64_t *out_count, hc_stream_t stream);
+
+/* Device buffers of one frame shape (reused across frames). */
+typedef struct {
+    float *terrain, *water;              /* [capacity][R][R] */
+    uint8_t *valid, *mask;               /* [capacity][R][R]; mask may be NULL */
+    uint8_t *patch_ok;                   /* [capacity][(R-1)^2] */
+    float *mip;                          /* [capacity][2][nodes(R)] */
+    int32_t *vrange;                     /* [capacity][2][2] */
+    void *mip_ws;                        /* hc_maxmip_workspace_bytes(2*capacity, R) */
+    size_t mip_ws_bytes;
+    uint8_t *rgb;                        /* [height][width][3] */
+    uint64_t *counters;                  /* [HC_COUNTERS], reset by hc_frame_launch */
+    uint32_t *tile_counter;
+    int32_t *tile_cost, *tile_order;     /* [hc_render_tiles(0,0,width,height)] */
+    int32_t capacity, resolution, width, height;
+} HcFrameBuffers;
+
+typedef struct {
+    double cm_lo, cm_hi;                 /* FrameConfig.colormap_range */
+    double light[3];                     /* unit _LIGHT_DIR (render.py:35-36) */
+    double stops[3][3];                  /* _COLOR_STOPS (render.py:32-34) */
+    uint8_t background[4];
+} HcShading;
+
+/* A whole frame from a host plan (hc_plan_cascades): descriptors for every cascade,
+ * then hc_discretize, hc_maxmip and hc_render on `stream`, counters reset first.
+ * events (optional, 4 cudaEvent_t): recorded before discretize, after discretize,
+ * after maxmip, after render.  rect (optional) = x0, y0, x1, y1 pixel sub-rectangle. */
+int hc_frame_launch(const HcPlan *plan, const HcCamera *cam, const HcDomain *dom, const HcGrid *grid,
+                    const HcFrameBuffers *buf, const HcShading *shade, const HcRenderDebug *dbg,
+                    const int32_t *rect, void *const *events, hc_stream_t stream);
 
 /* Self-test of the hoisted float64 division used by the traversal: counts operand
  * pairs (n pseudo-random + structured) where it differs from IEEE a / b. */

@@ -27,14 +27,39 @@ HC_OK, HC_EINVAL, HC_ECUDA, HC_ECAPACITY = 0, -1, -2, -3
 N_COUNTERS = 8
 
 # exported symbols, in header order (tests check the .so exports all of them)
-EXPORTS = ("hc_abi_version", "hc_last_error", "hc_build_records", "hc_visibility_mask",
+EXPORTS = ("hc_py_hypot", "hc_visible_hull", "hc_clip_cascades", "hc_fit_layout", "hc_plan_cascades",
+           "hc_abi_version", "hc_last_error", "hc_build_records", "hc_visibility_mask",
            "hc_discretize", "hc_maxmip_workspace_bytes", "hc_maxmip", "hc_render", "hc_render_tiles",
-           "hc_traverse_batch", "hc_eval_points", "hc_selftest_division")
+           "hc_traverse_batch", "hc_eval_points", "hc_frame_launch", "hc_selftest_division")
+HC_MAX_HULL = 64
 
 _vp = C.c_void_p
 _d = C.c_double
 _i32 = C.c_int32
 _i64 = C.c_int64
+
+
+class HcCamera(C.Structure):
+    _fields_ = [("eye", _d * 3), ("look", _d * 3), ("up", _d * 3), ("fov_y", _d), ("aspect", _d),
+                ("near_clip", _d), ("far_clip", _d)]
+
+
+class HcDomain(C.Structure):
+    _fields_ = [("xmin", _d), ("ymin", _d), ("xmax", _d), ("ymax", _d), ("h_lo", _d), ("h_hi", _d),
+                ("min_cell", _d)]
+
+
+class HcCascadePlan(C.Structure):
+    _fields_ = [("present", _i32), ("n_verts", _i32), ("verts", (_d * 2) * HC_MAX_EDGES),
+                ("near_offset", _d), ("far_offset", _d), ("origin", _d * 2), ("texel", _d),
+                ("resolution", _i32), ("box_texel", _i32 * 2), ("box_steps", _i32 * 2),
+                ("edges", (_d * 5) * HC_MAX_EDGES)]
+
+
+class HcPlan(C.Structure):
+    _fields_ = [("status", _i32), ("n_hull", _i32), ("hull", (_d * 2) * HC_MAX_HULL), ("overlap", _d),
+                ("axis_anchor", _d * 2), ("axis_dir", _d * 2), ("count", _i32), ("n_active", _i32),
+                ("c", HcCascadePlan * HC_MAX_CASCADES)]
 
 
 class HcGrid(C.Structure):
@@ -80,6 +105,34 @@ class HcRenderArgs(C.Structure):
                 ("tile_counter", _vp), ("tile_cost", _vp), ("tile_order", _vp), ("dbg", HcRenderDebug)]
 
 
+class HcFrameBuffers(C.Structure):
+    _fields_ = [("terrain", _vp), ("water", _vp), ("valid", _vp), ("mask", _vp), ("patch_ok", _vp),
+                ("mip", _vp), ("vrange", _vp), ("mip_ws", _vp), ("mip_ws_bytes", C.c_size_t), ("rgb", _vp),
+                ("counters", _vp), ("tile_counter", _vp), ("tile_cost", _vp), ("tile_order", _vp),
+                ("capacity", _i32), ("resolution", _i32), ("width", _i32), ("height", _i32)]
+
+
+class HcShading(C.Structure):
+    _fields_ = [("cm_lo", _d), ("cm_hi", _d), ("light", _d * 3), ("stops", _d * 9),
+                ("background", C.c_uint8 * 4)]
+
+
+ROOT_FN = C.CFUNCTYPE(C.c_double, C.c_double, C.c_int)
+
+
+def _numpy_root(q, count):
+    """The split ratio exactly as the reference evaluates it (cascade.py:306: np.cbrt)."""
+    import numpy as np
+    if count == 3:
+        return float(np.cbrt(q))
+    if count == 2:
+        return float(np.sqrt(q))
+    return float(np.power(q, 1.0 / count))
+
+
+NUMPY_ROOT = ROOT_FN(_numpy_root)
+
+
 class HeightcastCudaError(RuntimeError):
     """A libheightcast_cuda call failed (message from hc_last_error)."""
 
@@ -106,6 +159,13 @@ def lib():
     L = C.CDLL(LIB_PATH)
     L.hc_last_error.restype = C.c_char_p
     L.hc_abi_version.restype = C.c_int
+    L.hc_py_hypot.restype = C.c_double
+    L.hc_py_hypot.argtypes = [C.c_double, C.c_double]
+    L.hc_visible_hull.argtypes = [C.POINTER(HcCamera), C.POINTER(HcDomain), _vp, C.c_int, C.POINTER(C.c_int)]
+    L.hc_clip_cascades.argtypes = [_vp, C.c_int, _vp, C.c_double, _vp, C.c_int, ROOT_FN, C.POINTER(HcPlan)]
+    L.hc_fit_layout.argtypes = [_vp, C.c_int, C.c_int, C.c_double, C.c_double, C.POINTER(HcCascadePlan)]
+    L.hc_plan_cascades.argtypes = [C.POINTER(HcCamera), C.POINTER(HcDomain), C.c_int, C.c_double, C.c_int,
+                                   ROOT_FN, C.POINTER(HcPlan)]
     L.hc_maxmip_workspace_bytes.restype = C.c_size_t
     L.hc_maxmip_workspace_bytes.argtypes = [C.c_int, C.c_int]
     L.hc_build_records.argtypes = [C.POINTER(HcGrid), _vp, _vp, _vp, _vp, _vp]
@@ -116,6 +176,9 @@ def lib():
     L.hc_render.argtypes = [C.POINTER(HcRenderArgs), _vp]
     L.hc_traverse_batch.argtypes = [_vp, _vp, _vp, _vp, _vp, C.c_int, C.c_int] + [_vp] * 6 + \
         [_i64, _d, _d] + [_vp] * 6 + [_vp]
+    L.hc_frame_launch.argtypes = [C.POINTER(HcPlan), C.POINTER(HcCamera), C.POINTER(HcDomain), C.POINTER(HcGrid),
+                                  C.POINTER(HcFrameBuffers), C.POINTER(HcShading), C.POINTER(HcRenderDebug),
+                                  _vp, _vp, _vp]
     L.hc_render_tiles.restype = C.c_size_t
     L.hc_render_tiles.argtypes = [C.c_int] * 4
     L.hc_selftest_division.argtypes = [C.c_uint64, C.c_uint64, _vp, _vp]

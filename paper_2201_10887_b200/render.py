@@ -23,7 +23,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _cuda, _engine
-from .cascade import CameraView, NothingVisibleError, plan_cascades
+from .cascade import CameraView, NothingVisibleError, layouts_from_plan, plan_native
+from .cascade import _domain as _cascade_domain
 from .discretize import CascadeRaster
 from .grid import AdaptiveGrid, InfluenceTable
 from .rbf import RbfParams
@@ -155,29 +156,37 @@ def _background_frame(config, debug):
     return Frame(px, 0.0, 0.0, 0, 0, visible=False, debug={"visible": False} if debug else None)
 
 
+_SHADING: dict = {}
+
+
+def _shading(config):
+    key = (tuple(config.colormap_range), tuple(config.background))
+    s = _SHADING.get(key)
+    if s is None:
+        s = _SHADING[key] = _engine.shading(config.colormap_range, config.background)
+    return s
+
+
 def enqueue_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable,
                   settings: CascadeSettings = CascadeSettings(), debug: bool = False, rect=None):
-    """Plan on the host and enqueue one frame's kernels on the current stream.
+    """Plan natively on the host and enqueue one frame's kernels on the current stream.
 
-    Returns (buffers, plan) without waiting for the GPU, or None when nothing is
-    visible.  The device-resident half of `render_frame`; pixels stay in
-    `buffers.rgb` until read back."""
+    Returns (buffers, plan, plan_ms) without waiting for the GPU, or None when
+    nothing is visible.  The device-resident half of `render_frame`; pixels stay
+    in `buffers.rgb` until read back."""
     tp = time.perf_counter()
-    try:
-        hull, polygons, layouts = plan_cascades(config.camera, grid, settings.resolution,
-                                                settings.overlap, settings.count)
-    except NothingVisibleError:
+    plan = plan_native(config.camera, grid, settings.resolution, settings.overlap, settings.count)
+    if plan.status != 0:
         return None
     plan_ms = (time.perf_counter() - tp) * 1e3
-    active = [lay for lay in layouts if lay is not None]
     gdev = grid.device_view()
     ginf = gdev.influence(table)
-    buf = _frame_buffers(gdev.device, len(active), settings.resolution, config.width,
-                         config.height, debug)
-    fd = _engine.pack_frame(buf, active, config.camera, grid, config.width, config.height,
-                            config.colormap_range, config.background, rect=rect)
-    _engine.launch_frame(buf, fd, ginf, grid.height_range[0] - 1.0)
-    return buf, (hull, polygons, layouts, active, plan_ms)
+    buf = _frame_buffers(gdev.device, settings.count, settings.resolution, config.width, config.height, debug)
+    dom = getattr(grid, "_hc_domain", None)
+    if dom is None:
+        dom = grid._hc_domain = _cascade_domain(grid)
+    _engine.launch_planned(buf, plan, config.camera.native(), dom, ginf, _shading(config), rect=rect)
+    return buf, plan, plan_ms
 
 
 def render_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable, params: RbfParams,
@@ -192,7 +201,7 @@ def render_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable,
         queued = enqueue_frame(config, grid, table, settings, debug)
         if queued is None:
             return _background_frame(config, debug)
-        buf, (hull, polygons, layouts, active, plan_ms) = queued
+        buf, plan, plan_ms = queued
         pixels = torch.empty((config.height, config.width, 3), dtype=torch.uint8, pin_memory=True)
         pixels.copy_(buf.rgb, non_blocking=True)
         buf.counters_host.copy_(buf.counters, non_blocking=True)
@@ -208,6 +217,8 @@ def render_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable,
     frame.work = {"pairs": int(cnt[_cuda.CNT_PAIRS]), "node_visits": int(cnt[_cuda.CNT_NODE_VISITS]),
                   "patch_tests": int(cnt[_cuda.CNT_PATCH_TESTS])}
     if debug:
+        hull, polygons, layouts = layouts_from_plan(plan)
+        active = [lay for lay in layouts if lay is not None]
         for k, lay in enumerate(active):
             lay.mask = buf.mask[k].clone().bool()
         rasters = [CascadeRaster(lay, buf.terrain[k].clone(), buf.water[k].clone(),

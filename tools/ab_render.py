@@ -39,7 +39,7 @@ def child(cfg_name, frames, selftest):
     torch.cuda.synchronize()
     d, m, r = [], [], []
     for _ in range(frames):
-        buf, _plan = enqueue_frame(fc, g, t, st)
+        buf, _plan, _ms = enqueue_frame(fc, g, t, st)
         buf.ev[2].synchronize()
         d.append(buf.ev[0].elapsed_time(buf.ev[1]))
         m.append(buf.ev[1].elapsed_time(buf.ev[4]))
