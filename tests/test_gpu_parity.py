@@ -160,3 +160,64 @@ def test_approximate_fp64_matches_reference(cuda):
             assert abs(s.value - w[0]) <= 1e-12 * abs(w[0])
             assert abs(approximate(p, "water", g, t, P).value - w[1]) <= 1e-12 * abs(w[1])
             assert s.influencer_count == int(w[3])
+
+
+def _config_inputs(name, width=None, height=None):
+    from paper_2201_10887_b200 import build_influence_table
+    from paper_2201_10887_b200.configs import CONFIGS
+    from paper_2201_10887_b200.render import FrameConfig
+    cfg = CONFIGS[name]
+    g = cfg.grid()
+    t = build_influence_table(g, cfg.sigma)
+    fc = cfg.frame_config()
+    if width:
+        fc = FrameConfig(width=width, height=height, camera=fc.camera)
+    return cfg, g, t, fc
+
+
+@pytest.mark.parametrize("name,size", [("C1", None), ("C2", None), ("C3", (960, 540))])
+def test_benchmark_config_frame_parity(cuda, oracle, name, size):
+    """Full BASELINE configs: rays/traversal/resolve/shading bit-exact on the GPU's rasters,
+    masks and valid bits exact, heights within the float32 tolerance of the float64 oracle."""
+    from paper_2201_10887_b200 import render_frame
+    from paper_2201_10887_b200.rbf import RbfParams
+    cfg, g, t, fc = _config_inputs(name, *(size or (None, None)))
+    fr = render_frame(fc, g, t, RbfParams(sigma=cfg.sigma), cfg.settings(), debug=True)
+    assert fr.visible
+    _frame_vs_oracle(fr, oracle, fc, g)
+    lays = [L for L in fr.debug["layouts"] if L is not None]
+    assert len(lays) == cfg.cascades
+    worst = 0.0
+    for L, r in zip(lays, fr.debug["rasters"]):
+        o = oracle.discretize(L, g, t, cfg.sigma)
+        valid = _np(r.valid)
+        assert np.array_equal(valid, o.valid) and np.array_equal(_np(L.mask), o.mask)
+        for layer in ("terrain", "water"):
+            worst = max(worst, _check_heights(_np(r.layer(layer)), o.layer(layer), valid, f"{name} {layer}"))
+    print(f"{name}: max |dh| = {worst:.3e} m, rays_hit = {fr.rays_hit}")
+
+
+def test_division_selftest(cuda):
+    """The traversal's hoisted float64 division equals IEEE a / b on 2^28 operand pairs."""
+    import torch
+    from paper_2201_10887_b200 import _cuda
+    mm = torch.zeros(1, dtype=torch.int64, device=cuda)
+    _cuda.check(_cuda.lib().hc_selftest_division(1 << 28, 2024, mm.data_ptr(), _cuda.stream_ptr()), "selftest")
+    assert int(mm.item()) == 0
+
+
+def test_edge_cases_k_counts_and_nothing_visible(cuda, oracle):
+    """K = 1 / 2 / 8 cascades, tiny rasters, a camera looking away (background frame)."""
+    from paper_2201_10887_b200 import render_frame, CascadeSettings
+    from paper_2201_10887_b200.cascade import CameraView
+    from paper_2201_10887_b200.render import FrameConfig
+    from paper_2201_10887_b200.rbf import RbfParams
+    sc, g, t, cfg, st = demo_setup()
+    for K, R in ((1, 64), (2, 128), (8, 256), (5, 32)):
+        fr = render_frame(cfg, g, t, RbfParams(sigma=sc.sigma), CascadeSettings(resolution=R, count=K), debug=True)
+        _frame_vs_oracle(fr, oracle, cfg, g)
+    away = FrameConfig(width=64, height=48, camera=CameraView(eye=(-500.0, -500.0, 100.0), look_dir=(-1.0, -1.0, 0.5),
+                                                                up=(0, 0, 1), fov_y=30.0, aspect=64 / 48,
+                                                                near_clip=1.0, far_clip=100.0))
+    fr = render_frame(away, g, t, RbfParams(sigma=sc.sigma), st)
+    assert not fr.visible and np.all(fr.pixels == np.array(away.background, dtype=np.uint8))
