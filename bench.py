@@ -214,10 +214,19 @@ def main():
     from paper_2201_10887_b200.render import enqueue_frame
     from paper_2201_10887_b200.rbf import RbfParams
 
+    from paper_2201_10887_b200 import multi
+
     g, table, prep = build_inputs(cfg)
-    fc = rank_frame_config(cfg, rank, ws)
     st = cfg.settings()
     P = RbfParams(sigma=cfg.sigma)
+    strips = cfg.name == "C5"           # screen strips (strong scaling), else view sharding
+    if cfg.views > 1:
+        views = [cfg.frame_config(v) for v in multi.shard_views(cfg.views, ws, rank)]
+    else:
+        views = [rank_frame_config(cfg, 0 if strips else rank, ws)]
+    fc = views[0]
+    rects = multi.screen_strips(cfg.width, ws) if strips else None
+    rect = (rects[rank][0], 0, rects[rank][1], cfg.height) if strips else None
     t_up = time.perf_counter()
     gdev = g.device_view(dev)
     gdev.influence(table)
@@ -231,9 +240,12 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    def step(i):
+        return enqueue_frame(views[i % len(views)], g, table, st, rect=rect)
+
     # ---- warm-up (device-resident path)
-    for _ in range(max(args.warmup, 3)):
-        enqueue_frame(fc, g, table, st)
+    for i in range(max(args.warmup, 3)):
+        step(i)
     torch.cuda.synchronize()
 
     # ---- timed: K steps, each bracketed by CUDA events, L2 flushed between steps
@@ -245,7 +257,7 @@ def main():
             flush.zero_()
             torch.cuda.synchronize()
             ev[i][0].record()
-            buf, plan, plan_ms = enqueue_frame(fc, g, table, st)
+            buf, plan, plan_ms = step(i)
             ev[i][1].record()
             ev[i][1].synchronize()
             k_disc.append(buf.ev[0].elapsed_time(buf.ev[1]))
@@ -259,7 +271,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = ws * args.steps / (total_ms / 1e3)
+    frames_per_step = 1 if strips else ws
+    value = frames_per_step * args.steps / (total_ms / 1e3)
 
     cnt = buf.counters.cpu().tolist()
     work = {"pairs": cnt[_cuda.CNT_PAIRS], "node_visits": cnt[_cuda.CNT_NODE_VISITS],
@@ -267,15 +280,24 @@ def main():
             "visible_texels": cnt[_cuda.CNT_VISIBLE], "rays_hit": cnt[_cuda.CNT_RAYS_HIT]}
 
     # ---- e2e through the public API (pixels to pinned host memory every step)
-    for _ in range(2):
-        render_frame(fc, g, table, P, st)
+    def e2e_step(i):
+        if not strips:
+            render_frame(views[i % len(views)], g, table, P, st)
+            return
+        part = multi.render_strip(fc, g, table, P, st, rects[rank])
+        img = multi.gather_strips(part, rects, rank, ws) if ws > 1 else part
+        if rank == 0:
+            img.cpu()
+
+    for i in range(2):
+        e2e_step(i)
     barrier()
     e2e_ms = []
-    for _ in range(args.steps):
+    for i in range(args.steps):
         flush.zero_()
-        torch.cuda.synchronize()
+        barrier()
         t0 = time.perf_counter()
-        fr = render_frame(fc, g, table, P, st)
+        e2e_step(i)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     barrier()
     e2e_total = sum(e2e_ms)
@@ -283,7 +305,7 @@ def main():
         t = torch.tensor([e2e_total], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = float(t.item())
-    e2e_value = ws * args.steps / (e2e_total / 1e3)
+    e2e_value = frames_per_step * args.steps / (e2e_total / 1e3)
 
     # ---- rooflines (algorithmic work per launch / mean launch time)
     peaks, peak_kind = load_peaks()
@@ -337,14 +359,17 @@ def main():
         P_pix = cfg.width * cfg.height
         out = {
             "metric": "frames/sec", "value": value, "unit": "frames/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if strips else "weak",
             "vs_baseline": None, "dtype": "f64 traversal/shading, f32 RBF discretization", "data": "synthetic",
             "config": {"workload": f"{cfg.name}: {cfg.description}", "grid_cells": g.n_cells,
                        "mean_influence_list": round(len(table.indices) / g.n_cells, 2), "sigma": cfg.sigma,
                        "cascades": K, "cascade_res": R, "image": [cfg.width, cfg.height],
-                       "l2": "256 MiB flush between timed steps", "parallelism": f"view-sharded x{ws}"},
+                       "l2": "256 MiB flush between timed steps",
+                       "parallelism": f"screen strips x{ws}" if strips else f"view-sharded x{ws}",
+                       "views_per_rank": len(views)},
             "rays_per_sec": value * P_pix, "layer_rays_per_sec": value * 2 * P_pix,
-            "texels_per_sec": value * work["valid_texels"] / ws,
+            "texels_per_sec": value * work["valid_texels"] / frames_per_step,
             "e2e": {"value": e2e_value, "unit": "frames/s",
                     "h2d_bytes_per_step": _frame_param_bytes(K),
                     "d2h_bytes_per_step": P_pix * 3 + 8 * _cuda.N_COUNTERS,

@@ -221,3 +221,18 @@ def test_edge_cases_k_counts_and_nothing_visible(cuda, oracle):
                                                                 near_clip=1.0, far_clip=100.0))
     fr = render_frame(away, g, t, RbfParams(sigma=sc.sigma), st)
     assert not fr.visible and np.all(fr.pixels == np.array(away.background, dtype=np.uint8))
+
+
+def test_screen_strips_equal_full_frame(cuda):
+    """C5-style screen strips (each rank: full cascades, own pixel columns) reproduce the
+    single-GPU frame bit for bit."""
+    import torch
+    from paper_2201_10887_b200 import multi, render_frame
+    from paper_2201_10887_b200.rbf import RbfParams
+    sc, g, t, cfg, st = demo_setup()
+    full = render_frame(cfg, g, t, RbfParams(sigma=sc.sigma), st).pixels
+    for world in (2, 3, 8):
+        parts = [multi.render_strip(cfg, g, t, RbfParams(sigma=sc.sigma), st, r)
+                 for r in multi.screen_strips(cfg.width, world)]
+        img = torch.cat(parts, dim=1).cpu().numpy()
+        assert np.array_equal(img, full), world
