@@ -271,6 +271,32 @@ int hc_eval_points(const HcGrid *grid, const double *px, const double *py,
                    const int32_t *cells, int64_t n, double *out_t, double *out_w,
                    double *out_wsum, int64_t *out_count, hc_stream_t stream);
 
+/* ---- influence table on the GPU (grid.py:384-434) ----------------------- */
+
+#define HC_MAX_SIZE_CLASSES 32
+
+/* Cells binned per size class on a uniform grid (host counting sort). */
+typedef struct {
+    int32_t n_classes;
+    double xmin, ymin;                           /* bin grid origin (domain minimum) */
+    double class_size[HC_MAX_SIZE_CLASSES];      /* cell size of class s */
+    double bin_size[HC_MAX_SIZE_CLASSES];
+    int32_t nbx[HC_MAX_SIZE_CLASSES], nby[HC_MAX_SIZE_CLASSES];
+    int64_t class_bin_base[HC_MAX_SIZE_CLASSES]; /* class s's (nbx*nby + 1) bin starts in bin_start */
+    const int32_t *bin_start;                    /* device: absolute offsets into `cells` */
+    const int32_t *cells;                        /* device: cell ids sorted by (class, bin) */
+} HcInfluenceBins;
+
+size_t hc_influence_workspace_bytes(int n_cells);
+/* Two calls.  indices == NULL: counts + exclusive scan into offsets[n_cells+1]
+ * (device int64), *total_out (host) = number of entries.  Then with indices
+ * (device int64[total]): fill + per-list sort; *total_out (host, int32 view)
+ * receives 0, or the length of a list longer than the sort capacity (error).
+ * Both calls are stream-ordered; the host value is valid after a stream sync. */
+int hc_influence_build(const HcGrid *grid, const HcInfluenceBins *bins, double sigma, int64_t *offsets,
+                       int64_t *indices, int64_t capacity, void *workspace, size_t workspace_bytes,
+                       int64_t *total_out, hc_stream_t stream);
+
 /* Device buffers of one frame shape (reused across frames). */
 typedef struct {
     float *terrain, *water;              /* [capacity][R][R] */

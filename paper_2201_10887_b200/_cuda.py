@@ -30,7 +30,8 @@ N_COUNTERS = 8
 EXPORTS = ("hc_py_hypot", "hc_visible_hull", "hc_clip_cascades", "hc_fit_layout", "hc_plan_cascades",
            "hc_abi_version", "hc_last_error", "hc_build_records", "hc_visibility_mask",
            "hc_discretize", "hc_maxmip_workspace_bytes", "hc_maxmip", "hc_render", "hc_render_tiles",
-           "hc_traverse_batch", "hc_eval_points", "hc_frame_launch", "hc_selftest_division")
+           "hc_traverse_batch", "hc_eval_points", "hc_influence_workspace_bytes", "hc_influence_build",
+           "hc_frame_launch", "hc_selftest_division")
 HC_MAX_HULL = 64
 
 _vp = C.c_void_p
@@ -103,6 +104,16 @@ class HcRenderArgs(C.Structure):
                 ("cm_lo", _d), ("cm_hi", _d), ("stops", _d * 9), ("background", C.c_uint8 * 4),
                 ("c", HcRenderCascade * HC_MAX_CASCADES), ("rgb", _vp), ("counters", _vp),
                 ("tile_counter", _vp), ("tile_cost", _vp), ("tile_order", _vp), ("dbg", HcRenderDebug)]
+
+
+HC_MAX_SIZE_CLASSES = 32
+
+
+class HcInfluenceBins(C.Structure):
+    _fields_ = [("n_classes", _i32), ("xmin", _d), ("ymin", _d), ("class_size", _d * HC_MAX_SIZE_CLASSES),
+                ("bin_size", _d * HC_MAX_SIZE_CLASSES), ("nbx", _i32 * HC_MAX_SIZE_CLASSES),
+                ("nby", _i32 * HC_MAX_SIZE_CLASSES), ("class_bin_base", _i64 * HC_MAX_SIZE_CLASSES),
+                ("bin_start", _vp), ("cells", _vp)]
 
 
 class HcFrameBuffers(C.Structure):
@@ -179,6 +190,10 @@ def lib():
     L.hc_frame_launch.argtypes = [C.POINTER(HcPlan), C.POINTER(HcCamera), C.POINTER(HcDomain), C.POINTER(HcGrid),
                                   C.POINTER(HcFrameBuffers), C.POINTER(HcShading), C.POINTER(HcRenderDebug),
                                   _vp, _vp, _vp]
+    L.hc_influence_workspace_bytes.restype = C.c_size_t
+    L.hc_influence_workspace_bytes.argtypes = [C.c_int]
+    L.hc_influence_build.argtypes = [C.POINTER(HcGrid), C.POINTER(HcInfluenceBins), C.c_double, _vp, _vp,
+                                     C.c_int64, _vp, C.c_size_t, _vp, _vp]
     L.hc_render_tiles.restype = C.c_size_t
     L.hc_render_tiles.argtypes = [C.c_int] * 4
     L.hc_selftest_division.argtypes = [C.c_uint64, C.c_uint64, _vp, _vp]

@@ -18,6 +18,7 @@ Layout in HBM:
 from __future__ import annotations
 
 import ctypes as C
+import math
 
 import numpy as np
 
@@ -32,8 +33,12 @@ class InfluenceDevice:
             raise ValueError("influence table too large for int32 device indexing")
         self.table = table
         self.sigma = float(table.sigma)
-        self.offsets = torch.from_numpy(table.offsets.astype(np.int32)).to(dev)
-        self.indices = torch.from_numpy(table.indices.astype(np.int32)).to(dev)
+        cached = getattr(table, "_device_csr", {}).get(str(dev))
+        if cached is not None:        # built on this GPU: no re-upload
+            self.offsets, self.indices = cached
+        else:
+            self.offsets = torch.from_numpy(table.offsets.astype(np.int32)).to(dev)
+            self.indices = torch.from_numpy(table.indices.astype(np.int32)).to(dev)
         n_ent = max(len(table.indices), 1)
         n = gdev.n_cells
         self.rec4 = torch.empty((n_ent, 4), dtype=torch.float32, device=dev)
@@ -47,6 +52,76 @@ class InfluenceDevice:
                                                      self.anchor_d.data_ptr(),
                                                      _cuda.stream_ptr()), "hc_build_records")
         self.mean_list = float(len(table.indices)) / max(n, 1)
+
+
+def _size_class_bins(grid, sigma):
+    """Host counting sort of cells into one uniform bin grid per size class."""
+    sizes = grid.sizes
+    d = grid.domain
+    classes = np.unique(sizes)
+    if len(classes) > _cuda.HC_MAX_SIZE_CLASSES:
+        raise ValueError(f"{len(classes)} cell size classes (max {_cuda.HC_MAX_SIZE_CLASSES})")
+    cells, starts = [], []
+    base_cells = 0
+    base_bins = 0
+    B = _cuda.HcInfluenceBins()
+    B.n_classes = len(classes)
+    B.xmin, B.ymin = float(d.xmin), float(d.ymin)
+    for s, c in enumerate(classes.tolist()):
+        idx = np.flatnonzero(sizes == c)
+        bs = 3.5 * sigma * c + c                     # the reach spans ~3 bins per axis
+        nbx = int(math.floor(d.width / bs)) + 1
+        nby = int(math.floor(d.height / bs)) + 1
+        bx = np.clip(np.floor((grid.centers[idx, 0] - d.xmin) / bs).astype(np.int64), 0, nbx - 1)
+        by = np.clip(np.floor((grid.centers[idx, 1] - d.ymin) / bs).astype(np.int64), 0, nby - 1)
+        key = by * nbx + bx
+        order = np.argsort(key, kind="stable")
+        cells.append(idx[order].astype(np.int32))
+        counts = np.bincount(key, minlength=nby * nbx)
+        st = np.zeros(nby * nbx + 1, dtype=np.int64)
+        np.cumsum(counts, out=st[1:])
+        starts.append((st + base_cells).astype(np.int32))
+        B.class_size[s], B.bin_size[s], B.nbx[s], B.nby[s] = c, bs, nbx, nby
+        B.class_bin_base[s] = base_bins
+        base_cells += len(idx)
+        base_bins += nby * nbx + 1
+    return B, np.concatenate(cells), np.concatenate(starts)
+
+
+def build_influence_gpu(grid, sigma, device=None):
+    """grid.build_influence_table on the GPU (hc_influence_build); returns an
+    InfluenceTable with host CSR arrays and caches the device copy for the frame path."""
+    import torch
+    from .grid import InfluenceTable
+    gdev = grid.device_view(device)
+    dev = gdev.device
+    B, cells, starts = _size_class_bins(grid, sigma)
+    cells_d = torch.from_numpy(cells).to(dev)
+    starts_d = torch.from_numpy(starts).to(dev)
+    B.cells, B.bin_start = cells_d.data_ptr(), starts_d.data_ptr()
+    n = grid.n_cells
+    L = _cuda.lib()
+    ws = torch.empty(max(L.hc_influence_workspace_bytes(n), 16), dtype=torch.uint8, device=dev)
+    offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    total = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+    view = gdev.hc_grid()
+    with torch.cuda.device(dev):
+        s = _cuda.stream_ptr()
+        _cuda.check(L.hc_influence_build(C.byref(view), C.byref(B), sigma, offsets.data_ptr(), None, 0,
+                                         ws.data_ptr(), ws.numel(), total.data_ptr(), s), "hc_influence_build")
+        torch.cuda.current_stream().synchronize()
+        nnz = int(total.item())
+        indices = torch.empty(max(nnz, 1), dtype=torch.int64, device=dev)
+        flag = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+        _cuda.check(L.hc_influence_build(C.byref(view), C.byref(B), sigma, offsets.data_ptr(), indices.data_ptr(),
+                                         nnz, ws.data_ptr(), ws.numel(), flag.data_ptr(), s), "hc_influence_build")
+        torch.cuda.current_stream().synchronize()
+    over = int(flag.numpy().view(np.int32)[0])
+    if over:
+        raise _cuda.HeightcastCudaError(f"influence list of {over} entries exceeds the GPU sort capacity")
+    table = InfluenceTable(offsets.cpu().numpy(), indices[:nnz].cpu().numpy(), sigma)
+    table._device_csr = {str(dev): (offsets.to(torch.int32), indices[:nnz].to(torch.int32))}
+    return table
 
 
 class GridDevice:

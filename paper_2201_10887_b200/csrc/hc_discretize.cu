@@ -30,6 +30,9 @@ constexpr double NEG_HALF_LOG2E = -0.72134752044448170368;
 constexpr float Q_CUT = (float)(12.25 * NEG_HALF_LOG2E);
 // exp(-3.5^2 / 2) (rbf.py:30)
 constexpr float REMAINDER_F = 2.187491118182885e-03f;
+#ifndef DISC_BATCH
+#define DISC_BATCH 8
+#endif
 
 struct DiscretizeParams {
     HcCascadeRaster c[HC_MAX_CASCADES];
@@ -124,10 +127,7 @@ __global__ void __launch_bounds__(256) k_discretize(const __grid_constant__ Disc
         n_pairs = (unsigned)(end - beg);
         const float4* __restrict__ rec = reinterpret_cast<const float4*>(g.rec4);
         float wsum = 0.f, tn = 0.f, dn = 0.f;
-#pragma unroll 2
-        for (int j = beg; j < end; ++j) {
-            const float4 r = __ldg(rec + j);
-            const float dd = __ldg(g.rec_dd + j);
+        auto pair = [&](const float4& r, float dd) {
             const float dx = r.x - relx, dy = r.y - rely;
             const float q = fmaf(dx, dx, dy * dy) * r.z;
             const float e = ex2_approx(q) - REMAINDER_F;
@@ -135,7 +135,22 @@ __global__ void __launch_bounds__(256) k_discretize(const __grid_constant__ Disc
             wsum += w;
             tn = fmaf(w, r.w, tn);
             dn = fmaf(w, dd, dn);
+        };
+        // batches of DISC_BATCH records: all loads issued before the (in-order) accumulation,
+        // so each lane keeps 2*DISC_BATCH loads in flight instead of exposing one latency per pair
+        int j = beg;
+        for (; j + DISC_BATCH <= end; j += DISC_BATCH) {
+            float4 r[DISC_BATCH];
+            float dd[DISC_BATCH];
+#pragma unroll
+            for (int u = 0; u < DISC_BATCH; ++u) {
+                r[u] = __ldg(rec + j + u);
+                dd[u] = __ldg(g.rec_dd + j + u);
+            }
+#pragma unroll
+            for (int u = 0; u < DISC_BATCH; ++u) pair(r[u], dd[u]);
         }
+        for (; j < end; ++j) pair(__ldg(rec + j), __ldg(g.rec_dd + j));
         zero_w = !(wsum > 0.f);
         const float inv = 1.0f / wsum;
         ter = __ldg(g.anchor_t + a) + tn * inv;

@@ -31,10 +31,11 @@ def npz(name):
 
 def demo_setup():
     """Demo scene (scene.py:181-196) built with this package's host code."""
-    from paper_2201_10887_b200 import build_influence_table, scene
+    import heightcast_oracle as O
+    from paper_2201_10887_b200 import scene
     sc = scene.demo_scene()
     g = scene.scene_grid(sc)
-    t = build_influence_table(g, sc.sigma)
+    t = O.build_influence_table(g, sc.sigma)
     cfg = scene.scene_frame_config(sc)
     st = scene.scene_settings(sc)
     return sc, g, t, cfg, st

