@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define HC_ABI_VERSION 1
+#define HC_ABI_VERSION 2
 #define HC_MAX_EDGES 32      /* polygon edges per cascade mask          */
 #define HC_MAX_CASCADES 8    /* K (the reference hard-codes 3)           */
 #define HC_MAX_LEVELS 20     /* max-mip levels (R <= 2^19)               */
@@ -87,7 +87,9 @@ typedef struct {
     const float *heights;                /* [R][R] */
     const uint8_t *valid;                /* [R][R] */
     float *mip;                          /* flat levels, level L at level_off[L] */
-    uint8_t *patch_ok;                   /* [(R-1)^2] all four corners valid; may be NULL */
+    uint8_t *patch_ok;                   /* [(R-1)^2] bit 0: all four corners valid; bit 1: some
+                                          * corner differs from heights_other; may be NULL */
+    const float *heights_other;          /* the other layer's [R][R] heights for bit 1, or NULL */
     int32_t *vrange_key;                 /* [2] ordered-int min/max of valid heights */
     int32_t resolution;
     int32_t n_levels;
@@ -101,9 +103,13 @@ typedef struct {
     double rx, ry;                       /* (eye - origin) / texel, host-evaluated */
     double near_offset, far_offset;      /* polygon offsets along the view axis */
     int32_t resolution, n_levels;
+    int32_t patch_diff;                  /* nonzero: patch_ok bit 1 is set (hc_maxmip with
+                                          * heights_other = water) -- enables the exact
+                                          * water-layer reuse in hc_render */
+    int32_t reserved;
     const float *heights[2];             /* terrain, water [R][R] */
     const uint8_t *valid;                /* [R][R] */
-    const uint8_t *patch_ok;             /* [(R-1)^2], may be NULL */
+    const uint8_t *patch_ok;             /* [(R-1)^2] HcMipJob.patch_ok bits of the terrain job */
     const float *mip[2];                 /* terrain, water */
     const int32_t *vrange_key;           /* [2 layers][2] ordered-int min/max */
     int64_t level_off[HC_MAX_LEVELS];
@@ -123,6 +129,7 @@ typedef struct {
     double *raw_u, *raw_v;
     double *water_depth;                 /* [P]; NaN where the water layer missed */
     double *dirs;                        /* [P][3] */
+    int32_t *visits;                     /* [2][P] node visits per layer (0 for a reused water layer) */
 } HcRenderDebug;
 
 typedef struct {
@@ -139,7 +146,7 @@ typedef struct {
     HcRenderCascade c[HC_MAX_CASCADES];
     uint8_t *rgb;                        /* [height][width][3] (full-frame layout) */
     uint64_t *counters;                  /* HC_CNT_* (RAYS_HIT, NODE_VISITS, PATCH_TESTS), may be NULL */
-    /* persistent-warp tile queue over 4x4-pixel tiles of [x0,x1) x [y0,y1)
+    /* persistent-warp tile queue over 8x4-pixel tiles of [x0,x1) x [y0,y1)
      * (hc_render_tiles of them): */
     uint32_t *tile_counter;              /* queue head (device, 1 word), reset by hc_render   */
     int32_t *tile_cost;                  /* [tiles] in: previous launch's costs, out: this one's

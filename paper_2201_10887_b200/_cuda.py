@@ -17,7 +17,7 @@ LIB_DIR = os.path.join(PKG_DIR, "_lib")
 LIB_PATH = os.environ.get("HC_LIB_PATH") or os.path.join(LIB_DIR, "libheightcast_cuda.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 
-HC_ABI_VERSION = 1
+HC_ABI_VERSION = 2
 HC_MAX_EDGES = 32
 HC_MAX_CASCADES = 8
 HC_MAX_LEVELS = 20
@@ -79,21 +79,21 @@ class HcCascadeRaster(C.Structure):
 
 class HcMipJob(C.Structure):
     _fields_ = [("heights", _vp), ("valid", _vp), ("mip", _vp), ("patch_ok", _vp),
-                ("vrange_key", _vp), ("resolution", _i32), ("n_levels", _i32),
+                ("heights_other", _vp), ("vrange_key", _vp), ("resolution", _i32), ("n_levels", _i32),
                 ("level_off", _i64 * HC_MAX_LEVELS), ("level_w", _i32 * HC_MAX_LEVELS)]
 
 
 class HcRenderCascade(C.Structure):
     _fields_ = [("origin_x", _d), ("origin_y", _d), ("texel", _d), ("rx", _d), ("ry", _d),
                 ("near_offset", _d), ("far_offset", _d), ("resolution", _i32), ("n_levels", _i32),
-                ("heights", _vp * 2), ("valid", _vp), ("patch_ok", _vp), ("mip", _vp * 2),
+                ("patch_diff", _i32), ("reserved", _i32), ("heights", _vp * 2), ("valid", _vp), ("patch_ok", _vp), ("mip", _vp * 2),
                 ("vrange_key", _vp), ("level_off", _i64 * HC_MAX_LEVELS),
                 ("level_w", _i32 * HC_MAX_LEVELS)]
 
 
 class HcRenderDebug(C.Structure):
     _fields_ = [(n, _vp) for n in ("hit", "t", "near_k", "far_k", "w", "raw_t", "raw_ix", "raw_iy",
-                                   "raw_u", "raw_v", "water_depth", "dirs")]
+                                   "raw_u", "raw_v", "water_depth", "dirs", "visits")]
 
 
 class HcRenderArgs(C.Structure):

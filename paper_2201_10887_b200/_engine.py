@@ -59,7 +59,7 @@ def fill_cascade_raster(desc: _cuda.HcCascadeRaster, layout, terrain, water, val
     desc.mask = _cuda.ptr(mask)
 
 
-def fill_mip_job(job: _cuda.HcMipJob, R, heights, valid, mip, vrange_key, patch_ok=None):
+def fill_mip_job(job: _cuda.HcMipJob, R, heights, valid, mip, vrange_key, patch_ok=None, heights_other=None):
     off, w, _ = mip_shape(R)
     if len(off) > _cuda.HC_MAX_LEVELS:
         raise ValueError(f"raster resolution {R} needs {len(off)} mip levels (max {_cuda.HC_MAX_LEVELS})")
@@ -67,6 +67,7 @@ def fill_mip_job(job: _cuda.HcMipJob, R, heights, valid, mip, vrange_key, patch_
     job.valid = _cuda.ptr(valid)
     job.mip = _cuda.ptr(mip)
     job.patch_ok = _cuda.ptr(patch_ok)
+    job.heights_other = _cuda.ptr(heights_other)
     job.vrange_key = _cuda.ptr(vrange_key)
     job.resolution = R
     job.n_levels = len(off)
@@ -154,6 +155,7 @@ class FrameBuffers:
             "raw_v": torch.empty((2, 2, P), dtype=torch.float64, device=dev),
             "water_depth": torch.empty(P, dtype=torch.float64, device=dev),
             "dirs": torch.empty((P, 3), dtype=torch.float64, device=dev),
+            "visits": torch.empty((2, P), dtype=torch.int32, device=dev),
         }
         d = _cuda.HcRenderDebug()
         for name, t in self.dbg.items():

@@ -57,10 +57,13 @@ __global__ void __launch_bounds__(256) k_mip_tiles(const __grid_constant__ MipPa
         if (x < R && y < R) {
             const int64_t o = (int64_t)y * R + x;
             v = J.heights[o];
-            ok = J.valid[o];
+            ok = J.valid[o] != 0;
+            // bit 1: this texel differs from the other layer (bitwise: -0.0 vs 0.0 and NaNs
+            // count as different, so "same bits" implies every comparison agrees)
+            if (J.heights_other && __float_as_uint(J.heights_other[o]) != __float_as_uint(v)) ok |= 2;
             const bool own_x = tx < TILE || x == R - 1;
             const bool own_y = ty < TILE || y == R - 1;
-            if (ok && own_x && own_y) {
+            if ((ok & 1) && own_x && own_y) {
                 vmin = fminf(vmin, v);
                 vmax = fmaxf(vmax, v);
             }
@@ -78,9 +81,10 @@ __global__ void __launch_bounds__(256) k_mip_tiles(const __grid_constant__ MipPa
         if (x < n0 && y < n0) {
             m = fmaxf(fmaxf(h[ty][tx], h[ty][tx + 1]), fmaxf(h[ty + 1][tx], h[ty + 1][tx + 1]));
             J.mip[(int64_t)y * n0 + x] = m;
-            if (J.patch_ok)
-                J.patch_ok[(int64_t)y * n0 + x] =
-                    vv[ty][tx] & vv[ty][tx + 1] & vv[ty + 1][tx] & vv[ty + 1][tx + 1];
+            if (J.patch_ok) {
+                const uint8_t a = vv[ty][tx], b = vv[ty][tx + 1], c = vv[ty + 1][tx], e = vv[ty + 1][tx + 1];
+                J.patch_ok[(int64_t)y * n0 + x] = (uint8_t)((a & b & c & e & 1) | ((a | b | c | e) & 2));
+            }
         }
         lv[ty][tx] = m;
     }

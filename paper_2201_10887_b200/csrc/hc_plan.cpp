@@ -735,6 +735,7 @@ extern "C" int hc_frame_launch(const HcPlan* plan, const HcCamera* cam, const Hc
             j.valid = d.valid;
             j.mip = buf->mip + (2 * c + layer) * nodes;
             j.patch_ok = layer ? nullptr : buf->patch_ok + c * (int64_t)(R - 1) * (R - 1);
+            j.heights_other = layer ? nullptr : d.water;    // patch_ok bit 1 (water-layer reuse)
             j.vrange_key = buf->vrange + (2 * c + layer) * 2;
             j.resolution = R;
             j.n_levels = nlev;
@@ -755,6 +756,7 @@ extern "C" int hc_frame_launch(const HcPlan* plan, const HcCamera* cam, const Hc
         rc.heights[1] = d.water;
         rc.valid = d.valid;
         rc.patch_ok = jobs[2 * c].patch_ok;
+        rc.patch_diff = 1;
         rc.mip[0] = jobs[2 * c].mip;
         rc.mip[1] = jobs[2 * c + 1].mip;
         rc.vrange_key = buf->vrange + 4 * c;

@@ -24,6 +24,8 @@ from __future__ import annotations
 
 import numpy as np
 
+TILE_W, TILE_H = 8, 4          # render-kernel pixel tile (hc_render.cu TILE_W/TILE_H)
+
 
 def shard_views(n_views: int, world: int, rank: int) -> list[int]:
     """Round-robin view assignment for camera batches."""
@@ -37,7 +39,7 @@ def screen_strips(width: int, world: int, weights=None) -> list[tuple[int, int]]
 
     With `weights` (a per-column cost estimate, e.g. the previous frame's
     per-tile costs summed over rows) strips are cut at equal cumulative cost;
-    cuts are snapped to multiples of 4 pixels (the render kernel's tile width)."""
+    cuts are snapped to multiples of 8 pixels (the render kernel's tile width)."""
     if world < 1 or width < 1:
         raise ValueError("bad width/world")
     if weights is None:
@@ -48,15 +50,17 @@ def screen_strips(width: int, world: int, weights=None) -> list[tuple[int, int]]
             raise ValueError("weights must have one entry per pixel column")
         c = np.concatenate([[0.0], np.cumsum(np.maximum(w, 0.0) + 1e-12)])
         cuts = [int(np.searchsorted(c, c[-1] * r / world)) for r in range(world + 1)]
-    cuts = [min(width, max(0, 4 * round(x / 4))) for x in cuts]
+    cuts = [min(width, max(0, TILE_W * round(x / TILE_W))) for x in cuts]
     cuts[0], cuts[-1] = 0, width
     for i in range(1, len(cuts)):
         cuts[i] = max(cuts[i], cuts[i - 1])
     return [(cuts[r], cuts[r + 1]) for r in range(world)]
 
 
-def balance_strips(tile_cost, width: int, height: int, world: int, tile_w: int = 4, tile_h: int = 4):
+def balance_strips(tile_cost, width: int, height: int, world: int, tile_w: int = None, tile_h: int = None):
     """Strip cuts from a per-tile cost map (row-major tiles of tile_w x tile_h pixels)."""
+    tile_w = TILE_W if tile_w is None else tile_w
+    tile_h = TILE_H if tile_h is None else tile_h
     tx = (width + tile_w - 1) // tile_w
     ty = (height + tile_h - 1) // tile_h
     cost = np.asarray(tile_cost, dtype=np.float64)[:tx * ty].reshape(ty, tx).sum(axis=0)

@@ -230,6 +230,7 @@ def render_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable,
                        "terrain": LayerResolve(d, 0, len(active)),
                        "water": LayerResolve(d, 1, len(active)),
                        "dirs": d["dirs"].clone(), "water_depth": d["water_depth"].clone(),
+                       "visits": d["visits"].clone(),
                        "polygons": polygons, "hull": hull,
                        "mips": {"terrain": [buf.mip[k, 0].clone() for k in range(len(active))],
                                 "water": [buf.mip[k, 1].clone() for k in range(len(active))]},

@@ -27,7 +27,7 @@ def test_struct_layouts_match_header_sizes(native_lib_path):
     """ctypes mirrors of the ABI structs: field offsets follow C alignment rules."""
     from paper_2201_10887_b200 import _cuda
     assert C.sizeof(_cuda.HcCascadeRaster) == 8 * 3 + 4 * 2 + 8 * 160 + 8 * 4
-    assert C.sizeof(_cuda.HcMipJob) == 8 * 5 + 4 * 2 + 8 * 20 + 4 * 20
+    assert C.sizeof(_cuda.HcMipJob) == 8 * 6 + 4 * 2 + 8 * 20 + 4 * 20
     assert _cuda.HcRenderArgs.c.offset % 8 == 0 and _cuda.HcRenderArgs.dbg.offset % 8 == 0
 
 
@@ -43,7 +43,7 @@ def test_argument_validation_without_gpu(native_lib_path):
     assert L.hc_discretize(d, 99, C.byref(g), C.c_float(0.0), None, None) == _cuda.HC_EINVAL
     a = _cuda.HcRenderArgs()
     assert L.hc_render(C.byref(a), None) == _cuda.HC_EINVAL
-    assert L.hc_render_tiles(0, 0, 1920, 1080) == 480 * 270
+    assert L.hc_render_tiles(0, 0, 1920, 1080) == 240 * 270
     assert L.hc_maxmip_workspace_bytes(8, 1024) == 8 * 32 * 32 * 2 * 4
 
 
@@ -97,3 +97,30 @@ def test_influence_table_two_cells_boundary():
     import heightcast_oracle as O
     t = O.build_influence_table(g, 1.0)
     assert list(t.influencers(0)) == [0, 1] and list(t.influencers(1)) == [0, 1]
+
+
+def test_struct_field_offsets_match_c_compiler(tmp_path):
+    """Every ctypes field offset and struct size equals gcc's offsetof/sizeof on include/heightcast.h."""
+    import shutil
+    import subprocess
+    from paper_2201_10887_b200 import _cuda
+    cc = shutil.which("gcc") or "/usr/bin/gcc"
+    structs = [getattr(_cuda, n) for n in dir(_cuda)
+               if n.startswith("Hc") and isinstance(getattr(_cuda, n), type)
+               and issubclass(getattr(_cuda, n), C.Structure)]
+    assert len(structs) >= 10
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "heightcast.h"', "int main(void) {"]
+    want = []
+    for S in structs:
+        lines.append(f'printf("%zu\\n", sizeof({S.__name__}));')
+        want.append(C.sizeof(S))
+        for name, *_ in S._fields_:
+            lines.append(f'printf("%zu\\n", offsetof({S.__name__}, {name}));')
+            want.append(getattr(S, name).offset)
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run([cc, "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()]
+    assert got == want

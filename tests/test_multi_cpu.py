@@ -23,10 +23,11 @@ def test_screen_strips_partition_and_balance():
         s = multi.screen_strips(3840, world)
         assert s[0][0] == 0 and s[-1][1] == 3840
         assert all(a[1] == b[0] for a, b in zip(s, s[1:]))
-        assert all(x0 % 4 == 0 for x0, _ in s)
+        assert all(x0 % multi.TILE_W == 0 for x0, _ in s)
     # a cost map concentrated on the right half pushes the cuts right
-    cost = np.zeros((1080 // 4) * (1920 // 4))
-    cost.reshape(270, 480)[:, 240:] = 10.0
+    tw, th = multi.TILE_W, multi.TILE_H
+    cost = np.zeros((1080 // th) * (1920 // tw))
+    cost.reshape(1080 // th, 1920 // tw)[:, 960 // tw:] = 10.0
     s = multi.balance_strips(cost, 1920, 1080, 4)
     assert s[0][1] > 960 and s[-1][1] == 1920
 
