@@ -151,8 +151,8 @@ typedef struct {
     uint32_t *tile_counter;              /* queue head (device, 1 word), reset by hc_render   */
     int32_t *tile_cost;                  /* [tiles] in: previous launch's costs, out: this one's
                                           * (max node visits of a lane in the tile); may be NULL */
-    int32_t *tile_order;                 /* [tiles] scratch for the heaviest-first order; NULL =
-                                          * raster order (requires tile_cost when set) */
+    int32_t *tile_order;                 /* [hc_render_order_words] scratch for the heaviest-first
+                                          * order; NULL = raster order (requires tile_cost) */
     HcRenderDebug dbg;
 } HcRenderArgs;
 
@@ -258,8 +258,12 @@ int hc_maxmip(const HcMipJob *jobs, int n_jobs, void *workspace, size_t workspac
  * (render.py:100-110,125-186,189-341,249-256). */
 int hc_render(const HcRenderArgs *args, hc_stream_t stream);
 
-/* Number of 4x4-pixel tiles hc_render schedules for a pixel rectangle. */
+/* Number of 8x4-pixel tiles hc_render schedules for a pixel rectangle. */
 size_t hc_render_tiles(int x0, int y0, int x1, int y1);
+
+/* Size in int32 words of HcRenderArgs.tile_order for a pixel rectangle (the
+ * queue order plus the sort's per-chunk histograms). */
+size_t hc_render_order_words(int x0, int y0, int x1, int y1);
 
 /* Drop-in for the reference Numba kernel `_kernels.traverse_batch`
  * (_kernels.py:218-232): same arguments and per-lane outputs, device pointers,
@@ -316,7 +320,8 @@ typedef struct {
     uint8_t *rgb;                        /* [height][width][3] */
     uint64_t *counters;                  /* [HC_COUNTERS], reset by hc_frame_launch */
     uint32_t *tile_counter;
-    int32_t *tile_cost, *tile_order;     /* [hc_render_tiles(0,0,width,height)] */
+    int32_t *tile_cost;                  /* [hc_render_tiles(0,0,width,height)] */
+    int32_t *tile_order;                 /* [hc_render_order_words(0,0,width,height)] */
     int32_t capacity, resolution, width, height;
 } HcFrameBuffers;
 

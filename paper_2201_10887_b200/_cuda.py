@@ -30,7 +30,7 @@ N_COUNTERS = 8
 EXPORTS = ("hc_py_hypot", "hc_visible_hull", "hc_clip_cascades", "hc_fit_layout", "hc_plan_cascades",
            "hc_abi_version", "hc_last_error", "hc_build_records", "hc_visibility_mask",
            "hc_discretize", "hc_maxmip_workspace_bytes", "hc_maxmip", "hc_render", "hc_render_tiles",
-           "hc_traverse_batch", "hc_eval_points", "hc_influence_workspace_bytes", "hc_influence_build",
+           "hc_render_order_words", "hc_traverse_batch", "hc_eval_points", "hc_influence_workspace_bytes", "hc_influence_build",
            "hc_frame_launch", "hc_selftest_division")
 HC_MAX_HULL = 64
 
@@ -196,6 +196,8 @@ def lib():
                                      C.c_int64, _vp, C.c_size_t, _vp, _vp]
     L.hc_render_tiles.restype = C.c_size_t
     L.hc_render_tiles.argtypes = [C.c_int] * 4
+    L.hc_render_order_words.restype = C.c_size_t
+    L.hc_render_order_words.argtypes = [C.c_int] * 4
     L.hc_selftest_division.argtypes = [C.c_uint64, C.c_uint64, _vp, _vp]
     L.hc_eval_points.argtypes = [C.POINTER(HcGrid), _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
     ver = L.hc_abi_version()

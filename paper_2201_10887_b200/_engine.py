@@ -114,7 +114,8 @@ class FrameBuffers:
         self.rgb = torch.empty((H, W, 3), dtype=torch.uint8, device=dev)
         n_tiles = _cuda.lib().hc_render_tiles(0, 0, W, H)
         self.tile_cost = torch.zeros(max(n_tiles, 1), dtype=torch.int32, device=dev)
-        self.tile_order = torch.empty(max(n_tiles, 1), dtype=torch.int32, device=dev)
+        n_order = _cuda.lib().hc_render_order_words(0, 0, W, H)
+        self.tile_order = torch.empty(max(n_order, 1), dtype=torch.int32, device=dev)
         self.tile_counter = torch.zeros(1, dtype=torch.int32, device=dev)
         self.counters_host = torch.empty(_cuda.N_COUNTERS, dtype=torch.int64, pin_memory=True)
         self.dbg = None

@@ -44,6 +44,7 @@ def test_argument_validation_without_gpu(native_lib_path):
     a = _cuda.HcRenderArgs()
     assert L.hc_render(C.byref(a), None) == _cuda.HC_EINVAL
     assert L.hc_render_tiles(0, 0, 1920, 1080) == 240 * 270
+    assert L.hc_render_order_words(0, 0, 1920, 1080) == 240 * 270 + 32 * 16
     assert L.hc_maxmip_workspace_bytes(8, 1024) == 8 * 32 * 32 * 2 * 4
 
 
