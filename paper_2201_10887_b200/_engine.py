@@ -25,8 +25,8 @@ _L = np.array([-0.45, -0.35, 0.82])
 LIGHT_DIR = _L / np.linalg.norm(_L)               # render.py:35-36
 COLOR_STOPS = np.array([(0.0, 0.0, 128.0), (0.0, 180.0, 220.0), (240.0, 248.0, 255.0)])
 
-# hc_discretize (1) + hc_maxmip (2) + hc_render (2: tile order, render)
-LAUNCHES_PER_FRAME = 5
+# hc_discretize (1) + hc_maxmip (2) + hc_render (3: tile-order count + scatter, render)
+LAUNCHES_PER_FRAME = 6
 
 
 def mip_shape(R: int):
@@ -164,11 +164,20 @@ class FrameBuffers:
         self.dbg_native = d
 
 
-def launch_planned(buf: FrameBuffers, plan, camera_native, domain_native, ginf, shade, rect=None, stream=None):
-    """Enqueue one planned frame on `stream` (no host sync)."""
+def event_handles(events):
+    """hc_frame_launch event array from 4 torch events: before discretize, after
+    discretize, after maxmip (= before render), after render."""
+    return (C.c_void_p * 4)(*[e.cuda_event for e in events])
+
+
+def launch_planned(buf: FrameBuffers, plan, camera_native, domain_native, ginf, shade, rect=None, stream=None,
+                   events=None):
+    """Enqueue one planned frame on `stream` (no host sync).  `events`: optional
+    event_handles() array recorded instead of the buffers' own events."""
     r = None if rect is None else (C.c_int32 * 4)(*rect)
     _cuda.check(_cuda.lib().hc_frame_launch(
         C.byref(plan), C.byref(camera_native), C.byref(domain_native), C.byref(ginf.view), C.byref(buf.native),
         C.byref(shade), C.byref(buf.dbg_native) if buf.dbg_native is not None else None,
-        C.cast(r, C.c_void_p) if r is not None else None, C.cast(buf.ev_handles, C.c_void_p),
+        C.cast(r, C.c_void_p) if r is not None else None,
+        C.cast(buf.ev_handles if events is None else events, C.c_void_p),
         _cuda.stream_ptr(stream)), "hc_frame_launch")

@@ -168,7 +168,7 @@ def _shading(config):
 
 
 def enqueue_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable,
-                  settings: CascadeSettings = CascadeSettings(), debug: bool = False, rect=None):
+                  settings: CascadeSettings = CascadeSettings(), debug: bool = False, rect=None, events=None):
     """Plan natively on the host and enqueue one frame's kernels on the current stream.
 
     Returns (buffers, plan, plan_ms) without waiting for the GPU, or None when
@@ -185,7 +185,8 @@ def enqueue_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable
     dom = getattr(grid, "_hc_domain", None)
     if dom is None:
         dom = grid._hc_domain = _cascade_domain(grid)
-    _engine.launch_planned(buf, plan, config.camera.native(), dom, ginf, _shading(config), rect=rect)
+    _engine.launch_planned(buf, plan, config.camera.native(), dom, ginf, _shading(config), rect=rect,
+                           events=events)
     return buf, plan, plan_ms
 
 
