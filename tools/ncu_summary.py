@@ -90,7 +90,7 @@ def summarise(rep, tag, config):
     data = json.load(open(path)) if os.path.exists(path) else {}
     per = defaultdict(float)
     for short, r in kernels:
-        key = KERNEL_KEY.get(short)
+        key = KERNEL_KEY.get(short.replace("void ", "").split("<")[0].strip())
         if key is None:
             continue
         rd = to_float(r[col["dram__bytes_read.sum"]])
