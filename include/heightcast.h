@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define HC_ABI_VERSION 2
+#define HC_ABI_VERSION 3
 #define HC_MAX_EDGES 32      /* polygon edges per cascade mask          */
 #define HC_MAX_CASCADES 8    /* K (the reference hard-codes 3)           */
 #define HC_MAX_LEVELS 20     /* max-mip levels (R <= 2^19)               */
@@ -52,10 +52,14 @@ typedef void *hc_stream_t;   /* cudaStream_t */
 /* Device-resident adaptive grid + influence table.
  * grid.py:79-210 (SoA arrays, int32 min-cell tile index, -1 = hole) and
  * grid.py:350-434 (CSR influence lists, ascending, int32 on the device).
- * `rec4`/`rec_dd` are the anchored influence records built once per
- * (grid, sigma) by hc_build_records: for CSR entry j of cell a with influencer
- * i, rec4[j] = {cx_i - cx_a, cy_i - cy_a, -0.5*log2(e)/(sigma*size_i)^2,
- * terrain_i - terrain_a} and rec_dd[j] = depth_i - depth_a (float32). */
+ * The anchored influence records are built once per (grid, sigma) by
+ * hc_build_records.  For CSR entry j of cell a with influencer i the record is
+ * {x, y, s, t, d} = {cx_i - cx_a, cy_i - cy_a, -0.5*log2(e)/(sigma*size_i)^2,
+ * terrain_i - terrain_head, depth_i - depth_head} (float32), stored as pairs of
+ * consecutive list entries so two records feed one packed f32x2 operation:
+ * cell a's pairs are [pair_offsets[a], pair_offsets[a+1]), pair p of the list
+ * holding entries 2p and 2p+1 (an odd list's last pair is padded with a record
+ * of weight exactly 0). */
 typedef struct {
     const double *cx, *cy, *size, *terrain, *depth;   /* [n_cells] */
     const int32_t *tile_index;                         /* [nty][ntx] */
@@ -64,8 +68,10 @@ typedef struct {
     int32_t n_cells;
     const int32_t *offsets;                            /* [n_cells+1] */
     const int32_t *indices;                            /* [offsets[n]] */
-    const float *rec4;                                 /* [offsets[n]][4] */
-    const float *rec_dd;                               /* [offsets[n]] */
+    const int32_t *pair_offsets;                       /* [n_cells+1] prefix of ceil(list length / 2) */
+    const float *rec_xy;                               /* [pairs][4] {x0, x1, y0, y1} */
+    const float *rec_st;                               /* [pairs][4] {s0, s1, t0, t1} */
+    const float *rec_d;                                /* [pairs][2] {d0, d1} */
     const float *anchor_t, *anchor_d;                  /* [n_cells] terrain/depth of list head, f32 */
     double sigma;
 } HcGrid;
@@ -220,7 +226,7 @@ const char *hc_last_error(void);
 
 /* Anchored influence records from the CSR table (startup precompute; replaces the
  * per-batch gather of discretize.py:111-119 + rbf.py:109-123 operand setup). */
-int hc_build_records(const HcGrid *grid, float *rec4, float *rec_dd, float *anchor_t,
+int hc_build_records(const HcGrid *grid, float *rec_xy, float *rec_st, float *rec_d, float *anchor_t,
                      float *anchor_d, hc_stream_t stream);
 
 /* Visibility mask only (cascade.py:507-521).  mask is [R][R] uint8. */

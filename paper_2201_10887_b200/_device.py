@@ -10,8 +10,9 @@ Layout in HBM:
   tile_index                     int32 [nty, ntx]  min-cell lookup (grid.py:154-177)
   offsets                        int32 [N+1]       CSR (grid.py:350-376)
   indices                        int32 [N*L]
-  rec4                           float32 [N*L, 4]  (dx, dy, exp scale, d_terrain) per entry
-  rec_dd                         float32 [N*L]     d_depth per entry
+  pair_offsets                   int32 [N+1]       prefix of ceil(list length / 2)
+  rec_xy, rec_st                 float32 [pairs, 4] {x0, x1, y0, y1}, {s0, s1, t0, t1}
+  rec_d                          float32 [pairs, 2] {d0, d1}  (pairs of consecutive list entries)
   anchor_t, anchor_d             float32 [N]       list-head terrain / depth
 """
 
@@ -39,16 +40,24 @@ class InfluenceDevice:
         else:
             self.offsets = torch.from_numpy(table.offsets.astype(np.int32)).to(dev)
             self.indices = torch.from_numpy(table.indices.astype(np.int32)).to(dev)
-        n_ent = max(len(table.indices), 1)
         n = gdev.n_cells
-        self.rec4 = torch.empty((n_ent, 4), dtype=torch.float32, device=dev)
-        self.rec_dd = torch.empty(n_ent, dtype=torch.float32, device=dev)
+        lens = np.diff(np.asarray(table.offsets, dtype=np.int64))
+        pair_off = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum((lens + 1) // 2, out=pair_off[1:])
+        if pair_off[-1] >= 2 ** 31:
+            raise ValueError("influence table too large for int32 device indexing")
+        self.pair_offsets = torch.from_numpy(pair_off.astype(np.int32)).to(dev)
+        n_pairs = max(int(pair_off[-1]), 1)
+        self.rec_xy = torch.empty((n_pairs, 4), dtype=torch.float32, device=dev)
+        self.rec_st = torch.empty((n_pairs, 4), dtype=torch.float32, device=dev)
+        self.rec_d = torch.empty((n_pairs, 2), dtype=torch.float32, device=dev)
         self.anchor_t = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
         self.anchor_d = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
         self.view = gdev.hc_grid(self)
         with torch.cuda.device(dev):
-            _cuda.check(_cuda.lib().hc_build_records(C.byref(self.view), self.rec4.data_ptr(),
-                                                     self.rec_dd.data_ptr(), self.anchor_t.data_ptr(),
+            _cuda.check(_cuda.lib().hc_build_records(C.byref(self.view), self.rec_xy.data_ptr(),
+                                                     self.rec_st.data_ptr(), self.rec_d.data_ptr(),
+                                                     self.anchor_t.data_ptr(),
                                                      self.anchor_d.data_ptr(),
                                                      _cuda.stream_ptr()), "hc_build_records")
         self.mean_list = float(len(table.indices)) / max(n, 1)
@@ -160,7 +169,8 @@ class GridDevice:
         g.n_cells = self.n_cells
         if inf is not None:
             g.offsets, g.indices = inf.offsets.data_ptr(), inf.indices.data_ptr()
-            g.rec4, g.rec_dd = inf.rec4.data_ptr(), inf.rec_dd.data_ptr()
+            g.pair_offsets = inf.pair_offsets.data_ptr()
+            g.rec_xy, g.rec_st, g.rec_d = inf.rec_xy.data_ptr(), inf.rec_st.data_ptr(), inf.rec_d.data_ptr()
             g.anchor_t, g.anchor_d = inf.anchor_t.data_ptr(), inf.anchor_d.data_ptr()
             g.sigma = inf.sigma
         return g

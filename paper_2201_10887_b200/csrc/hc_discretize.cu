@@ -7,17 +7,29 @@
 //   discretize.py:79-108    grouped Eq. 2 evaluation with sentinel / valid
 //   rbf.py:77-130           truncated-Gaussian weights + anchored sums
 //
-// Design (B200): one thread per texel, warps own 8x4 texel tiles so a warp's
-// lanes almost always share one containing cell and therefore one influence
-// list: every record load is a warp-wide broadcast and the loop trip count is
-// warp-uniform.  Each CSR entry is a precomputed 20-byte anchored record
-// (hc_build_records): the influencer's centre relative to the containing
-// cell's centre, the Gaussian exponent scale, and value differences to the
-// list head (the reference's anchor, rbf.py:119-123).  The texel's offset to
-// its cell centre is computed in float64 and rounded once, so the float32
-// distance keeps ~1 ulp relative accuracy on 2 km domains.  exp is one MUFU
-// ex2 per pair.  Per-texel summation order is the list order, so rasters are
-// deterministic and independent of the launch shape.
+// Design (B200): one thread per texel, warps own 8x4 texel tiles, blocks 16x16.
+//  * Block classification: a block whose texels provably all fail (or all pass)
+//    the mask's edge tests skips the per-texel float64 tests (classify_block);
+//    86 % of C3's cascade texels lie outside the mask polygon.
+//  * Records: each CSR entry is a precomputed anchored record (hc_build_records):
+//    the influencer's centre relative to the containing cell's centre, the
+//    Gaussian exponent scale, and value differences to the list head (the
+//    reference's anchor, rbf.py:119-123), stored as pairs of consecutive entries
+//    so two records feed one packed f32x2 FADD2/FMUL2/FFMA2 (same per-element
+//    rounding as scalar code).  The texel's offset to its cell centre is computed
+//    in float64 and rounded once, so float32 distances keep ~1 ulp relative
+//    accuracy on 2 km domains.  exp is one MUFU ex2 per record.
+//  * Warps whose texels fall in at most STAGE_GROUPS cells (C3: 91 % of warps)
+//    stream those cells' lists cooperatively -- coalesced cp.async copies of 64
+//    record pairs per chunk into a per-warp double buffer in shared memory, the
+//    next chunk in flight while the current one is consumed -- and every lane
+//    reads its own cell's records from shared memory.  With per-lane loads all
+//    lanes of such a warp fetch the same address, keeping only a few hundred
+//    bytes in flight per warp (C3 ran DRAM-latency-bound at ~1.3 TB/s).
+//  * Other warps gather per lane (32 distinct lists in flight), after an
+//    asynchronous bulk L2 prefetch of each lane's whole list.
+// Per-texel summation order is the list order, so rasters are deterministic and
+// independent of the launch shape.
 #include <math.h>
 
 #include "hc_internal.cuh"
@@ -31,8 +43,37 @@ constexpr float Q_CUT = (float)(12.25 * NEG_HALF_LOG2E);
 // exp(-3.5^2 / 2) (rbf.py:30)
 constexpr float REMAINDER_F = 2.187491118182885e-03f;
 #ifndef DISC_BATCH
-#define DISC_BATCH 8
+#define DISC_BATCH 4               // record pairs per batch of the per-lane path
 #endif
+constexpr int STAGE_PAIRS = 64;    // record pairs per warp buffer, shared by up to STAGE_GROUPS cells
+#ifndef DISC_STAGE_GROUPS
+#define DISC_STAGE_GROUPS 8
+#endif
+constexpr int STAGE_GROUPS = DISC_STAGE_GROUPS;
+constexpr int DISC_WARPS = 8;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// asynchronous DRAM -> L2 prefetch of a byte range (TMA unit; no registers, no completion)
+__device__ __forceinline__ void prefetch_l2(const void* p, int bytes) {
+    const uintptr_t a0 = (uintptr_t)p & ~(uintptr_t)15;
+    const uintptr_t a1 = ((uintptr_t)p + (uintptr_t)bytes + 15) & ~(uintptr_t)15;
+    if (a1 > a0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 struct DiscretizeParams {
     HcCascadeRaster c[HC_MAX_CASCADES];
@@ -43,8 +84,12 @@ struct DiscretizeParams {
 
 // ---------------------------------------------------------------------------
 
-__global__ void __launch_bounds__(256) k_build_records(HcGrid g, float4* __restrict__ rec4,
-                                                       float* __restrict__ rec_dd,
+// Pair-interleaved anchored records (see heightcast.h HcGrid): one warp per cell,
+// one lane per record pair; an odd list's last pair gets a neutral second record
+// (x = 1e15, scale = -1e30: q = -inf, weight exactly 0, t = d = 0) so the pair loop
+// needs no tail and the sums are unchanged bit for bit.
+__global__ void __launch_bounds__(256) k_build_records(HcGrid g, float4* __restrict__ rec_xy,
+                                                       float4* __restrict__ rec_st, float2* __restrict__ rec_d,
                                                        float* __restrict__ anchor_t,
                                                        float* __restrict__ anchor_d) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -52,6 +97,7 @@ __global__ void __launch_bounds__(256) k_build_records(HcGrid g, float4* __restr
     if (warp >= g.n_cells) return;
     const int a = warp;
     const int beg = g.offsets[a], end = g.offsets[a + 1];
+    const int pbeg = g.pair_offsets[a], pend = g.pair_offsets[a + 1];
     const int head = g.indices[beg];
     const double cxa = g.cx[a], cya = g.cy[a];
     const double th = g.terrain[head], dh = g.depth[head];
@@ -59,16 +105,26 @@ __global__ void __launch_bounds__(256) k_build_records(HcGrid g, float4* __restr
         anchor_t[a] = (float)th;
         anchor_d[a] = (float)dh;
     }
-    for (int j = beg + lane; j < end; j += 32) {
-        const int i = g.indices[j];
-        const double cs = g.size[i] * g.sigma;
-        float4 r;
-        r.x = (float)(g.cx[i] - cxa);
-        r.y = (float)(g.cy[i] - cya);
-        r.z = (float)(NEG_HALF_LOG2E / (cs * cs));
-        r.w = (float)(g.terrain[i] - th);
-        rec4[j] = r;
-        rec_dd[j] = (float)(g.depth[i] - dh);
+    for (int p = pbeg + lane; p < pend; p += 32) {
+        float x[2], y[2], sc[2], t[2], d[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int j = beg + 2 * (p - pbeg) + k;
+            if (j < end) {
+                const int i = g.indices[j];
+                const double cs = g.size[i] * g.sigma;
+                x[k] = (float)(g.cx[i] - cxa);
+                y[k] = (float)(g.cy[i] - cya);
+                sc[k] = (float)(NEG_HALF_LOG2E / (cs * cs));
+                t[k] = (float)(g.terrain[i] - th);
+                d[k] = (float)(g.depth[i] - dh);
+            } else {
+                x[k] = 1e15f, y[k] = 0.f, sc[k] = -1e30f, t[k] = 0.f, d[k] = 0.f;
+            }
+        }
+        rec_xy[p] = make_float4(x[0], x[1], y[0], y[1]);
+        rec_st[p] = make_float4(sc[0], sc[1], t[0], t[1]);
+        rec_d[p] = make_float2(d[0], d[1]);
     }
 }
 
@@ -100,6 +156,45 @@ __global__ void __launch_bounds__(256) k_visibility_mask(HcCascadeRaster c) {
     c.mask[(int64_t)iy * c.resolution + ix] = texel_visible(c, px, py) ? 1 : 0;
 }
 
+// Classify a block of texels [x0, x1] x [y0, y1] against the mask polygon without
+// testing every texel (86 % of C3's cascade texels lie outside the polygon).  The
+// computed texel centres are monotone in the index, so they lie in the box spanned
+// by the corner centres; each edge test is the rounded value of a linear function
+// L(p) = e_x (p_y - a_y) - e_y (p_x - a_x), whose extremes over the box are at the
+// corners, and every rounded evaluation (texel or corner) is within
+// 2^-45 (|e_x|(|p_y|+|a_y|) + |e_y|(|p_x|+|a_x|)) of L (three roundings of at most
+// 2^-53 relative each).  An edge that fails at all four corners by more than twice
+// that bound fails for every texel; an edge that passes by that margin everywhere
+// passes for every texel.  Returns 0 = all outside, 1 = all inside, 2 = test texels.
+__device__ int classify_block(const HcCascadeRaster& c, int x0, int y0, int x1, int y1, int lane) {
+    const double qx0 = dadd(c.origin_x, dmul((double)x0, c.texel)), qx1 = dadd(c.origin_x, dmul((double)x1, c.texel));
+    const double qy0 = dadd(c.origin_y, dmul((double)y0, c.texel)), qy1 = dadd(c.origin_y, dmul((double)y1, c.texel));
+    bool fail_all = false, pass_all = true;
+    for (int e0 = 0; e0 < c.n_edges; e0 += 32) {
+        const int e = e0 + lane;
+        bool fail = false, pass = true;
+        if (e < c.n_edges) {
+            const double* E = c.edges[e];
+            double lo = INFINITY, hi = -INFINITY, mag = 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double px = (k & 1) ? qx1 : qx0, py = (k & 2) ? qy1 : qy0;
+                const double cr = dsub(dmul(E[2], dsub(py, E[1])), dmul(E[3], dsub(px, E[0])));
+                lo = fmin(lo, cr);
+                hi = fmax(hi, cr);
+                mag = fmax(mag, dadd(dmul(fabs(E[2]), dadd(fabs(py), fabs(E[1]))),
+                                     dmul(fabs(E[3]), dadd(fabs(px), fabs(E[0])))));
+            }
+            const double tol = dmul(mag, 0x1p-44);
+            fail = dadd(hi, tol) < E[4];
+            pass = dsub(lo, tol) >= E[4];
+        }
+        fail_all |= __any_sync(0xffffffffu, fail);
+        pass_all &= __all_sync(0xffffffffu, pass);
+    }
+    return fail_all ? 0 : (pass_all ? 1 : 2);
+}
+
 __global__ void __launch_bounds__(256) k_discretize(const __grid_constant__ DiscretizeParams P,
                                                     const __grid_constant__ HcGrid g) {
     const HcCascadeRaster& c = P.c[blockIdx.z];
@@ -110,47 +205,175 @@ __global__ void __launch_bounds__(256) k_discretize(const __grid_constant__ Disc
     const int iy = blockIdx.y * 16 + (warp >> 1) * 4 + (lane >> 3);
     if (blockIdx.x * 16 >= (unsigned)R || blockIdx.y * 16 >= (unsigned)R) return;
     const bool in_raster = ix < R && iy < R;
+    const int64_t o = (int64_t)iy * R + ix;
 
+    __shared__ int s_cls;
+    if (warp == 0) {
+        const int cls = classify_block(c, blockIdx.x * 16, blockIdx.y * 16, min((int)blockIdx.x * 16 + 15, R - 1),
+                                       min((int)blockIdx.y * 16 + 15, R - 1), lane);
+        if (lane == 0) s_cls = cls;
+    }
+    __syncthreads();
+    const int cls = s_cls;
+    if (cls == 0) {                        // whole block outside the mask polygon
+        if (in_raster) {
+            c.terrain[o] = P.sentinel;
+            c.water[o] = P.sentinel;
+            c.valid[o] = 0;
+            if (c.mask) c.mask[o] = 0;
+        }
+        return;
+    }
     const double px = dadd(c.origin_x, dmul((double)ix, c.texel));
     const double py = dadd(c.origin_y, dmul((double)iy, c.texel));
-    const bool vis = in_raster && texel_visible(c, px, py);
+    const bool vis = in_raster && (cls == 1 || texel_visible(c, px, py));
     const int a = vis ? containing_cell(g, px, py) : -1;
-    const int64_t o = (int64_t)iy * R + ix;
 
     float ter = P.sentinel, wat = P.sentinel;
     bool zero_w = false;
     unsigned n_pairs = 0;
+    __shared__ __align__(16) float4 s_xy[DISC_WARPS][2][STAGE_PAIRS + STAGE_GROUPS];
+    __shared__ __align__(16) float4 s_st[DISC_WARPS][2][STAGE_PAIRS + STAGE_GROUPS];
+    __shared__ __align__(16) float2 s_d[DISC_WARPS][2][STAGE_PAIRS + STAGE_GROUPS];
+
+    // distinct cells of the warp (up to STAGE_GROUPS): lane t < ng holds group t's pair range
+    const unsigned FULL = 0xffffffffu;
+    unsigned rem = __ballot_sync(FULL, a >= 0);
+    const bool any_valid = rem != 0u;
+    int gid = -1, ng = 0, g_beg = 0, g_end = 0;
+#pragma unroll
+    for (int t = 0; t < STAGE_GROUPS; ++t) {
+        if (rem) {
+            const int cell = __shfl_sync(FULL, a, __ffs(rem) - 1);
+            const unsigned m = __ballot_sync(FULL, a == cell);
+            if (a == cell) gid = t;
+            if (lane == t) {
+                g_beg = __ldg(g.pair_offsets + cell);
+                g_end = __ldg(g.pair_offsets + cell + 1);
+            }
+            rem &= ~m;
+            ng = t + 1;
+        }
+    }
+    const bool staged = any_valid && rem == 0u;
+
+    float wsum = 0.f, tn = 0.f, dn = 0.f;
+#ifdef DISC_PACKED_SUMS
+    float2 ws2 = make_float2(0.f, 0.f), tn2 = ws2, dn2 = ws2;
+#endif
+    float2 nrel = make_float2(0.f, 0.f), nrely = make_float2(0.f, 0.f);
     if (a >= 0) {
         const float relx = (float)dsub(px, g.cx[a]);
         const float rely = (float)dsub(py, g.cy[a]);
-        const int beg = __ldg(g.offsets + a), end = __ldg(g.offsets + a + 1);
-        n_pairs = (unsigned)(end - beg);
-        const float4* __restrict__ rec = reinterpret_cast<const float4*>(g.rec4);
-        float wsum = 0.f, tn = 0.f, dn = 0.f;
-        auto pair = [&](const float4& r, float dd) {
-            const float dx = r.x - relx, dy = r.y - rely;
-            const float q = fmaf(dx, dx, dy * dy) * r.z;
-            const float e = ex2_approx(q) - REMAINDER_F;
-            const float w = (q > Q_CUT) ? fmaxf(e, 0.f) : 0.f;
-            wsum += w;
-            tn = fmaf(w, r.w, tn);
-            dn = fmaf(w, dd, dn);
+        nrel = make_float2(-relx, -relx);
+        nrely = make_float2(-rely, -rely);
+        n_pairs = (unsigned)(__ldg(g.offsets + a + 1) - __ldg(g.offsets + a));
+    }
+    // one record pair: the two records' Eq. 1 terms with packed f32x2 arithmetic
+    // (same per-element operations and rounding as the scalar form), then the
+    // sums in list order
+    auto pair2 = [&](const float4& xy, const float4& st, const float2& dd) {
+        const float2 dx = __fadd2_rn(make_float2(xy.x, xy.y), nrel);
+        const float2 dy = __fadd2_rn(make_float2(xy.z, xy.w), nrely);
+        const float2 q = __fmul2_rn(__ffma2_rn(dx, dx, __fmul2_rn(dy, dy)), make_float2(st.x, st.y));
+        const float e0 = ex2_approx(q.x) - REMAINDER_F, e1 = ex2_approx(q.y) - REMAINDER_F;
+        const float w0 = (q.x > Q_CUT) ? fmaxf(e0, 0.f) : 0.f;
+        const float w1 = (q.y > Q_CUT) ? fmaxf(e1, 0.f) : 0.f;
+#ifdef DISC_PACKED_SUMS
+        const float2 w = make_float2(w0, w1);
+        ws2 = __fadd2_rn(ws2, w);
+        tn2 = __ffma2_rn(w, make_float2(st.z, st.w), tn2);
+        dn2 = __ffma2_rn(w, dd, dn2);
+#else
+        wsum += w0;
+        wsum += w1;
+        tn = fmaf(w0, st.z, tn);
+        tn = fmaf(w1, st.w, tn);
+        dn = fmaf(w0, dd.x, dn);
+        dn = fmaf(w1, dd.y, dn);
+#endif
+    };
+    const float4* __restrict__ gxy = reinterpret_cast<const float4*>(g.rec_xy);
+    const float4* __restrict__ gst = reinterpret_cast<const float4*>(g.rec_st);
+    const float2* __restrict__ gd = reinterpret_cast<const float2*>(g.rec_d);
+    if (staged) {
+        // group slots of chg pairs (+1 pad: groups start in different banks)
+        const int lg = 6 - (32 - __clz(ng - 1));      // 64 / next_pow2(ng) pairs per group
+        const int chg = 1 << lg;
+        const int maxlen = __reduce_max_sync(FULL, (unsigned)(lane < ng ? g_end - g_beg : 0));
+        const int nchunks = (maxlen + chg - 1) >> lg;
+        auto issue = [&](int k, int buf) {
+#pragma unroll
+            for (int i = 0; i < STAGE_PAIRS / 32; ++i) {
+                const int r = i * 32 + lane;
+                const int gg = r >> lg, idx = r & (chg - 1);
+                const int gb = __shfl_sync(FULL, g_beg, gg), ge = __shfl_sync(FULL, g_end, gg);
+                const int src = gb + (k << lg) + idx;
+                if (gg < ng && src < ge) {
+                    const int dst = gg * (chg + 1) + idx;
+                    cp_async16(&s_xy[warp][buf][dst], gxy + src);
+                    cp_async16(&s_st[warp][buf][dst], gst + src);
+                    cp_async8(&s_d[warp][buf][dst], gd + src);
+                }
+            }
+            cp_async_commit();
         };
-        // batches of DISC_BATCH records: all loads issued before the (in-order) accumulation,
-        // so each lane keeps 2*DISC_BATCH loads in flight instead of exposing one latency per pair
+        const int gsel = gid >= 0 ? gid : 0;
+        const int mb = __shfl_sync(FULL, g_beg, gsel), me = __shfl_sync(FULL, g_end, gsel);
+        const int mylen = gid >= 0 ? me - mb : 0;
+        const int myoff = gsel * (chg + 1);
+        issue(0, 0);
+        for (int k = 0; k < nchunks; ++k) {
+            if (k + 1 < nchunks) {
+                issue(k + 1, (k + 1) & 1);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncwarp();
+            const float4* XY = &s_xy[warp][k & 1][myoff];
+            const float4* ST = &s_st[warp][k & 1][myoff];
+            const float2* D = &s_d[warp][k & 1][myoff];
+            const int n = min(chg, mylen - (k << lg));
+            int u = 0;
+            for (; u + 4 <= n; u += 4) {
+#pragma unroll
+                for (int v = 0; v < 4; ++v) pair2(XY[u + v], ST[u + v], D[u + v]);
+            }
+            for (; u < n; ++u) pair2(XY[u], ST[u], D[u]);
+            __syncwarp();                  // buffer k & 1 is refilled at step k + 1
+        }
+    } else if (a >= 0) {
+        const int beg = __ldg(g.pair_offsets + a), end = __ldg(g.pair_offsets + a + 1);
+#ifndef DISC_NO_L2_PREFETCH
+        // lanes of this path walk different lists: start streaming each whole list into
+        // L2 at once so the batched loads below wait for L2 rather than DRAM
+        prefetch_l2(gxy + beg, (end - beg) * 16);
+        prefetch_l2(gst + beg, (end - beg) * 16);
+        prefetch_l2(gd + beg, (end - beg) * 8);
+#endif
+        // batches of DISC_BATCH pairs: all loads issued before the (in-order) accumulation
         int j = beg;
         for (; j + DISC_BATCH <= end; j += DISC_BATCH) {
-            float4 r[DISC_BATCH];
-            float dd[DISC_BATCH];
+            float4 xy[DISC_BATCH], st[DISC_BATCH];
+            float2 dd[DISC_BATCH];
 #pragma unroll
             for (int u = 0; u < DISC_BATCH; ++u) {
-                r[u] = __ldg(rec + j + u);
-                dd[u] = __ldg(g.rec_dd + j + u);
+                xy[u] = __ldg(gxy + j + u);
+                st[u] = __ldg(gst + j + u);
+                dd[u] = __ldg(gd + j + u);
             }
 #pragma unroll
-            for (int u = 0; u < DISC_BATCH; ++u) pair(r[u], dd[u]);
+            for (int u = 0; u < DISC_BATCH; ++u) pair2(xy[u], st[u], dd[u]);
         }
-        for (; j < end; ++j) pair(__ldg(rec + j), __ldg(g.rec_dd + j));
+        for (; j < end; ++j) pair2(__ldg(gxy + j), __ldg(gst + j), __ldg(gd + j));
+    }
+#ifdef DISC_PACKED_SUMS
+    wsum = ws2.x + ws2.y;
+    tn = tn2.x + tn2.y;
+    dn = dn2.x + dn2.y;
+#endif
+    if (a >= 0) {
         zero_w = !(wsum > 0.f);
         const float inv = 1.0f / wsum;
         ter = __ldg(g.anchor_t + a) + tn * inv;
@@ -222,14 +445,16 @@ __global__ void k_eval_points(HcGrid g, const double* __restrict__ px, const dou
 
 using namespace hc;
 
-extern "C" int hc_build_records(const HcGrid* grid, float* rec4, float* rec_dd, float* anchor_t,
+extern "C" int hc_build_records(const HcGrid* grid, float* rec_xy, float* rec_st, float* rec_d, float* anchor_t,
                                 float* anchor_d, hc_stream_t stream) {
-    HC_REQUIRE(grid && rec4 && rec_dd && anchor_t && anchor_d, "hc_build_records: null argument");
+    HC_REQUIRE(grid && rec_xy && rec_st && rec_d && anchor_t && anchor_d, "hc_build_records: null argument");
+    HC_REQUIRE(grid->offsets && grid->indices && grid->pair_offsets, "hc_build_records: grid without CSR");
     HC_REQUIRE(grid->n_cells >= 0, "hc_build_records: negative cell count");
     if (grid->n_cells == 0) return HC_OK;
     const int blocks = (int)(((int64_t)grid->n_cells * 32 + 255) / 256);
     k_build_records<<<blocks, 256, 0, (cudaStream_t)stream>>>(
-        *grid, reinterpret_cast<float4*>(rec4), rec_dd, anchor_t, anchor_d);
+        *grid, reinterpret_cast<float4*>(rec_xy), reinterpret_cast<float4*>(rec_st),
+        reinterpret_cast<float2*>(rec_d), anchor_t, anchor_d);
     return cuda_status("hc_build_records");
 }
 
@@ -260,7 +485,8 @@ extern "C" int hc_discretize(const HcCascadeRaster* cascades, int n_cascades, co
         P.c[k] = c;
         rmax = c.resolution > rmax ? c.resolution : rmax;
     }
-    HC_REQUIRE(grid->rec4 && grid->rec_dd && grid->offsets && grid->tile_index,
+    HC_REQUIRE(grid->rec_xy && grid->rec_st && grid->rec_d && grid->pair_offsets && grid->offsets &&
+                   grid->tile_index,
                "hc_discretize: grid records not built");
     P.n_cascades = n_cascades;
     P.sentinel = sentinel;
