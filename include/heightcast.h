@@ -219,6 +219,22 @@ int hc_fit_layout(const double *verts_xy, int n, int resolution, double min_cell
 int hc_plan_cascades(const HcCamera *cam, const HcDomain *dom, int resolution, double overlap, int count,
                      hc_root_fn root, HcPlan *out);
 
+/* ---- AHF text parser (grid.py:236-331 load_grid) ---- */
+
+typedef struct {
+    double xmin, ymin, xmax, ymax, min_cell;  /* header values */
+    int64_t count;                       /* declared (and present) cell count */
+    int64_t error_line;                  /* 1-based line of the error, 0 if none */
+    int32_t non_ascii;                   /* text has non-ASCII bytes: not parsed (caller's parser) */
+    int32_t reserved;
+} HcAhfInfo;
+
+/* Host-only.  Parses ASCII AHF text with load_grid's grammar, checks, messages
+ * and line numbers.  cells == NULL: header and structure only (sets count);
+ * otherwise fills cells[count][5] = {cx, cy, size, terrain, water_depth}.
+ * HC_EINVAL with hc_last_error() + info->error_line on malformed input. */
+int hc_ahf_parse(const char *text, int64_t len, HcAhfInfo *info, double *cells, int64_t capacity);
+
 /* ---- entry points ------------------------------------------------------ */
 
 int hc_abi_version(void);

@@ -30,8 +30,8 @@ N_COUNTERS = 8
 EXPORTS = ("hc_py_hypot", "hc_visible_hull", "hc_clip_cascades", "hc_fit_layout", "hc_plan_cascades",
            "hc_abi_version", "hc_last_error", "hc_build_records", "hc_visibility_mask",
            "hc_discretize", "hc_maxmip_workspace_bytes", "hc_maxmip", "hc_render", "hc_render_tiles",
-           "hc_render_order_words", "hc_traverse_batch", "hc_eval_points", "hc_influence_workspace_bytes", "hc_influence_build",
-           "hc_frame_launch", "hc_selftest_division")
+           "hc_render_order_words", "hc_traverse_batch", "hc_eval_points", "hc_influence_workspace_bytes",
+           "hc_influence_build", "hc_frame_launch", "hc_selftest_division", "hc_ahf_parse")
 HC_MAX_HULL = 64
 
 _vp = C.c_void_p
@@ -124,6 +124,11 @@ class HcFrameBuffers(C.Structure):
                 ("capacity", _i32), ("resolution", _i32), ("width", _i32), ("height", _i32)]
 
 
+class HcAhfInfo(C.Structure):
+    _fields_ = [("xmin", _d), ("ymin", _d), ("xmax", _d), ("ymax", _d), ("min_cell", _d),
+                ("count", _i64), ("error_line", _i64), ("non_ascii", _i32), ("reserved", _i32)]
+
+
 class HcShading(C.Structure):
     _fields_ = [("cm_lo", _d), ("cm_hi", _d), ("light", _d * 3), ("stops", _d * 9),
                 ("background", C.c_uint8 * 4)]
@@ -201,6 +206,7 @@ def lib():
     L.hc_render_order_words.argtypes = [C.c_int] * 4
     L.hc_selftest_division.argtypes = [C.c_uint64, C.c_uint64, _vp, _vp]
     L.hc_eval_points.argtypes = [C.POINTER(HcGrid), _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
+    L.hc_ahf_parse.argtypes = [C.c_char_p, _i64, C.POINTER(HcAhfInfo), _vp, _i64]
     ver = L.hc_abi_version()
     if ver != HC_ABI_VERSION:
         raise HeightcastCudaError(f"libheightcast_cuda ABI {ver}, expected {HC_ABI_VERSION}")

@@ -1,0 +1,83 @@
+"""Native AHF parser (hc_ahf_parse) against the Python restatement of load_grid
+(grid.py:236-331): same grids, same GridFormatError messages and line numbers."""
+
+import numpy as np
+import pytest
+
+from paper_2201_10887_b200.grid import GridFormatError, _load_grid_text, load_grid
+from paper_2201_10887_b200.synth import generate_synthetic
+
+GOOD = "AHF 1\ndomain 0 0 8 8\nmin_cell 4\ncells 4\n2 2 4 10 0\n6 2 4 11 0.5\n2 6 4 12 0\n6 6 4 13 1.25\n"
+
+
+def _same(a, b):
+    assert (a.domain.xmin, a.domain.ymin, a.domain.xmax, a.domain.ymax) == \
+        (b.domain.xmin, b.domain.ymin, b.domain.xmax, b.domain.ymax)
+    assert a.min_cell_size == b.min_cell_size
+    for x, y in ((a.centers, b.centers), (a.sizes, b.sizes), (a.terrain, b.terrain),
+                 (a.water_depth, b.water_depth)):
+        assert np.array_equal(np.asarray(x).view(np.uint64), np.asarray(y).view(np.uint64))
+
+
+def _outcome(fn, text):
+    try:
+        # bytes for load_grid: a str without a newline would be read as a path
+        return ("ok", fn(text.encode("ascii") if fn is load_grid else text))
+    except GridFormatError as e:
+        return ("err", str(e), e.line)
+
+
+@pytest.mark.parametrize("text", [
+    GOOD,
+    GOOD.replace("\n", "\r\n"),
+    GOOD.replace("\n", "\r"),
+    "# comment\n\n  " + GOOD.replace("cells 4", "  cells  +0_4 ") + "\n# trailing\n\n",
+    GOOD.replace("2 2 4 10 0", "2.0 2e0 4_0e-1_0 1.0e1 -0.0").replace("min_cell 4", "min_cell 0.4e1"),
+    GOOD.replace("6 6 4 13 1.25", "6 6 4 inf NaN").replace("domain 0 0 8 8", "domain -0 .0 8. +8"),
+    GOOD.replace("\n", "\x0b", 2),
+    GOOD.replace("\n", "\x1c\n", 1),
+])
+def test_native_parser_matches_python_on_valid_text(text):
+    a, b = _outcome(load_grid, text), _outcome(_load_grid_text, text)
+    assert a[0] == b[0], (a, b)
+    if a[0] == "ok":
+        _same(a[1], b[1])
+    else:
+        assert a[1:] == b[1:]
+
+
+@pytest.mark.parametrize("text", [
+    "",
+    "\n\n",
+    "AHF 2\n",
+    "AHF 1\ndomain 0 0 8\n",
+    "AHF 1\ndomain 0 0 8 x\n",
+    "AHF 1\ndomain 0 0 0 8\n",
+    "AHF 1\ndomain 0 0 8 8\nmin_cell\n",
+    "AHF 1\ndomain 0 0 8 8\nmin_cell 1__0\n",
+    "AHF 1\ndomain 0 0 8 8\nmin_cell -1\n",
+    "AHF 1\ndomain 0 0 8 8\nmin_cell 4\ncells 1.5\n",
+    "AHF 1\ndomain 0 0 8 8\nmin_cell 4\ncells -3\n",
+    "AHF 1\ndomain 0 0 8 8\nmin_cell 4\ncells 0007\n1 1 1 1 1\n",
+    "AHF 1\ndomain 0 0 8 8\nmin_cell 4\ncells 99999999999999999999999\n",
+    GOOD + "2 2 4 10 0\n",
+    GOOD.replace("6 2 4 11 0.5", "6 2 4 11"),
+    GOOD.replace("6 2 4 11 0.5", "6 2 4 11 0x1p3"),
+    GOOD.replace("6 2 4 11 0.5", "6 2 4 11 1e"),
+    GOOD.replace("6 2 4 11 0.5", "6 2 4 11 _1"),
+    GOOD.replace("6 2 4 11 0.5", "6 2 4 11 1_"),
+    GOOD.replace("6 2 4 11 0.5", "6 2 4 11 infinit"),
+])
+def test_native_parser_matches_python_on_malformed_text(text):
+    a, b = _outcome(load_grid, text), _outcome(_load_grid_text, text)
+    assert a[0] == b[0] == "err", (a, b)
+    assert a[1:] == b[1:]
+
+
+def test_native_parser_round_trips_a_synthetic_grid(tmp_path):
+    g = generate_synthetic("pond", 3, 2000)
+    path = tmp_path / "g.ahf"
+    g.save(str(path))
+    text = path.read_text()
+    _same(load_grid(str(path)), _load_grid_text(text))
+    _same(load_grid(str(path)), g)
