@@ -235,6 +235,13 @@ typedef struct {
  * HC_EINVAL with hc_last_error() + info->error_line on malformed input. */
 int hc_ahf_parse(const char *text, int64_t len, HcAhfInfo *info, double *cells, int64_t capacity);
 
+/* Host-only.  The min-cell tile index (grid.py:154-177 _paint_tiles): index is
+ * int32 [nty][ntx], filled with -1 and then with each cell's id over its
+ * (x0, y0, span) tile square in cell order; clash[2] = (earlier cell, later cell)
+ * of the first overlap or (-1, -1); stop_on_overlap ends painting there. */
+int hc_paint_tiles(const int64_t *x0, const int64_t *y0, const int64_t *span, int64_t n, int64_t ntx,
+                   int64_t nty, int stop_on_overlap, int32_t *index, int64_t *clash);
+
 /* ---- entry points ------------------------------------------------------ */
 
 int hc_abi_version(void);

@@ -1,4 +1,7 @@
-// hc_ahf.cpp -- AHF text parser: load_grid's per-line Python
+// hc_ahf.cpp -- grid ingestion on the host: the AHF parser and
+// the tile-index painter.
+//
+// AHF text parser: load_grid's per-line Python
 // loop (grid.py:236-331) in C++.  Same grammar, same checks in the same order,
 // same messages and 1-based line numbers, for ASCII text:
 //   * lines split like Python's str.splitlines (\n, \r\n, \r, \v, \f, \x1c-\x1e),
@@ -16,6 +19,7 @@
 #include <string.h>
 #include <strings.h>
 
+#include <algorithm>
 #include <charconv>
 #include <string>
 #include <vector>
@@ -265,6 +269,46 @@ extern "C" int hc_ahf_parse(const char* text, int64_t len, HcAhfInfo* info, doub
         if (nt != 5) return fail(info, r.no, "expected 5 values per cell line");
         for (int k = 0; k < 5; ++k)
             if (!py_float(t[k], cells[5 * c + k])) return fail(info, r.no, "cell values are not numbers");
+    }
+    return HC_OK;
+}
+
+// grid.py:154-177 (_paint_tiles): cells painted into the min-cell tile index in
+// cell order, each over index[max(y0,0):y0+span, max(x0,0):x0+span] with numpy's
+// slice semantics; the first cell found already painted (row-major) under a later
+// cell is the reported clash, and with stop_on_overlap painting ends there.
+namespace {
+int64_t slice_stop(int64_t stop, int64_t dim) {
+    if (stop < 0) stop = stop + dim < 0 ? 0 : stop + dim;
+    return stop > dim ? dim : stop;
+}
+}  // namespace
+
+extern "C" int hc_paint_tiles(const int64_t* x0, const int64_t* y0, const int64_t* span, int64_t n, int64_t ntx,
+                              int64_t nty, int stop_on_overlap, int32_t* index, int64_t* clash) {
+    if ((n > 0 && (!x0 || !y0 || !span)) || !index || !clash || ntx < 1 || nty < 1) {
+        hc::set_error("hc_paint_tiles: bad argument");
+        return HC_EINVAL;
+    }
+    std::fill(index, index + ntx * nty, -1);
+    clash[0] = clash[1] = -1;
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t ya = y0[i] > 0 ? y0[i] : 0, yb = slice_stop(y0[i] + span[i], nty);
+        const int64_t xa = x0[i] > 0 ? x0[i] : 0, xb = slice_stop(x0[i] + span[i], ntx);
+        if (ya >= yb || xa >= xb) continue;
+        if (clash[0] < 0) {
+            for (int64_t y = ya; y < yb && clash[0] < 0; ++y) {
+                const int32_t* row = index + y * ntx;
+                for (int64_t x = xa; x < xb; ++x)
+                    if (row[x] >= 0) {
+                        clash[0] = row[x];
+                        clash[1] = i;
+                        break;
+                    }
+            }
+            if (clash[0] >= 0 && stop_on_overlap) return HC_OK;
+        }
+        for (int64_t y = ya; y < yb; ++y) std::fill(index + y * ntx + xa, index + y * ntx + xb, (int32_t)i);
     }
     return HC_OK;
 }

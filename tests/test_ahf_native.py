@@ -81,3 +81,25 @@ def test_native_parser_round_trips_a_synthetic_grid(tmp_path):
     text = path.read_text()
     _same(load_grid(str(path)), _load_grid_text(text))
     _same(load_grid(str(path)), g)
+
+
+@pytest.mark.parametrize("kind,seed,cells", [("pond", 7, 3000), ("hill", 1, 800), ("ramp", 0, 1024)])
+def test_native_tile_painter_matches_numpy(kind, seed, cells):
+    g = generate_synthetic(kind, seed, cells)
+    for stop in (True, False):
+        a, ca = g._paint(stop)
+        b, cb = g._paint_numpy(stop)
+        assert np.array_equal(a, b) and ca == cb
+
+
+def test_native_tile_painter_reports_overlaps_like_numpy():
+    from paper_2201_10887_b200.grid import AdaptiveGrid, Rect
+    centers = np.array([[2.0, 2.0], [4.0, 4.0], [6.0, 6.0], [2.0, 6.0]])
+    sizes = np.array([4.0, 4.0, 4.0, 4.0])
+    z = np.zeros(4)
+    g = AdaptiveGrid(Rect(0, 0, 8, 8), 2.0, centers, sizes, z + 10, z, check_overlap=False)
+    for stop in (True, False):
+        a, ca = g._paint(stop)
+        b, cb = g._paint_numpy(stop)
+        assert ca == cb == (0, 1)
+        assert np.array_equal(a, b)
