@@ -8,9 +8,10 @@ GPU mask + RBF discretization, max mipmaps, ray casting and shading.
 `value`  : frames/s with the grid resident in HBM, each step timed with CUDA
            events on the launching stream (host planning included, since the GPU
            waits for it), L2 flushed (256 MiB write) between timed steps.
-`e2e`    : frames/s through the public API `render_frame(...)` (host-planned,
-           kernel descriptors copied host->device as launch parameters, pixels
-           read back into pinned host memory), host wall clock per call.
+`e2e`    : frames/s through the public API `render_frames(...)` (every frame
+           host-planned, kernel descriptors copied host->device as launch
+           parameters, pixels read back into pinned host memory on a copy stream
+           overlapping the next frame), host wall clock over the K frames.
 `roofline`: the dominant kernel's algorithmic work per launch / its mean event
            duration vs MEASURED_PEAKS.json (see DESIGN.md for the unit models).
 `cpu_baseline`: the float64 C oracle port of the reference pipeline
@@ -48,7 +49,7 @@ MUFU_PER_SM_CLK = 16          # ex2 lanes per SM per clock (SURVEY.md §8 d)
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
@@ -247,7 +248,6 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
-    from paper_2201_10887_b200 import render_frame
     from paper_2201_10887_b200 import _cuda, _engine
     from paper_2201_10887_b200.render import enqueue_frame
     from paper_2201_10887_b200.rbf import RbfParams
@@ -326,26 +326,37 @@ def main():
             "patch_tests": cnt[_cuda.CNT_PATCH_TESTS], "valid_texels": cnt[_cuda.CNT_VALID],
             "visible_texels": cnt[_cuda.CNT_VISIBLE], "rays_hit": cnt[_cuda.CNT_RAYS_HIT]}
 
-    # ---- e2e through the public API (pixels to pinned host memory every step)
-    def e2e_step(i):
-        if not strips:
-            render_frame(views[i % len(views)], g, table, P, st)
-            return
-        part = multi.render_strip(fc, g, table, P, st, rects[rank])
-        img = multi.gather_strips(part, rects, rank, ws) if ws > 1 else part
-        if rank == 0:
-            img.cpu()
-
-    for i in range(2):
-        e2e_step(i)
-    barrier()
-    e2e_ms = []
-    for i in range(args.steps):
-        flush.zero_()
+    # ---- e2e through the public API, host wall clock: every frame planned on the host,
+    # its descriptors passed to the GPU, its pixels read back into pinned host memory.
+    # Views: render_frames (read-back of frame i overlaps frame i+1), an L2 flush
+    # enqueued before every frame.  Strips: render_strip + image gather per step.
+    if not strips:
+        from paper_2201_10887_b200 import render_frames
+        seq = [views[i % len(views)] for i in range(args.steps)]
+        for _ in render_frames(seq[:2] * 4, g, table, P, st):      # both buffer sets, pinned blocks
+            pass
         barrier()
         t0 = time.perf_counter()
-        e2e_step(i)
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        for _ in render_frames(seq, g, table, P, st, before_frame=lambda i: flush.zero_()):
+            pass
+        e2e_ms = [(time.perf_counter() - t0) * 1e3]
+    else:
+        def e2e_step(i):
+            part = multi.render_strip(fc, g, table, P, st, rects[rank])
+            img = multi.gather_strips(part, rects, rank, ws) if ws > 1 else part
+            if rank == 0:
+                img.cpu()
+
+        for i in range(2):
+            e2e_step(i)
+        barrier()
+        e2e_ms = []
+        for i in range(args.steps):
+            flush.zero_()
+            barrier()
+            t0 = time.perf_counter()
+            e2e_step(i)
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
     barrier()
     e2e_total = sum(e2e_ms)
     if ws > 1:

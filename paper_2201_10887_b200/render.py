@@ -136,11 +136,12 @@ class LayerResolve:
 
 
 _BUFFERS: dict = {}
+_COPY_STREAMS: dict = {}       # per device: read-back stream of render_frames
 
 
-def _frame_buffers(device, K, R, W, H, debug):
+def _frame_buffers(device, K, R, W, H, debug, slot=0):
     import torch
-    key = (str(device), K, R, W, H, bool(debug))
+    key = (str(device), K, R, W, H, bool(debug), int(slot))
     buf = _BUFFERS.get(key)
     if buf is None:
         if len(_BUFFERS) > 8:
@@ -168,7 +169,8 @@ def _shading(config):
 
 
 def enqueue_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable,
-                  settings: CascadeSettings = CascadeSettings(), debug: bool = False, rect=None, events=None):
+                  settings: CascadeSettings = CascadeSettings(), debug: bool = False, rect=None, events=None,
+                  slot: int = 0):
     """Plan natively on the host and enqueue one frame's kernels on the current stream.
 
     Returns (buffers, plan, plan_ms) without waiting for the GPU, or None when
@@ -181,7 +183,8 @@ def enqueue_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable
     plan_ms = (time.perf_counter() - tp) * 1e3
     gdev = grid.device_view()
     ginf = gdev.influence(table)
-    buf = _frame_buffers(gdev.device, settings.count, settings.resolution, config.width, config.height, debug)
+    buf = _frame_buffers(gdev.device, settings.count, settings.resolution, config.width, config.height, debug,
+                         slot)
     dom = getattr(grid, "_hc_domain", None)
     if dom is None:
         dom = grid._hc_domain = _cascade_domain(grid)
@@ -208,7 +211,69 @@ def render_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable,
         buf.counters_host.copy_(buf.counters, non_blocking=True)
         buf.ev[3].record()
         buf.ev[3].synchronize()
-    cnt = buf.counters_host.tolist()
+    return _finish_frame(buf, plan, plan_ms, pixels, buf.counters_host, grid, params, debug)
+
+
+def render_frames(configs, grid: AdaptiveGrid, table: InfluenceTable, params: RbfParams,
+                  settings: CascadeSettings = CascadeSettings(), before_frame=None):
+    """Render a sequence of frames (a camera path or a batch of views), yielding
+    one `Frame` per config, identical to `render_frame`'s.
+
+    Frames alternate between two device buffer sets; frame i's pixels are read
+    back on a copy stream while frame i+1 is planned and computed, so the host
+    planning and the read-back overlap the GPU work.  `before_frame(i)`, if given,
+    is called before frame i is enqueued (e.g. to enqueue an L2 flush)."""
+    import torch
+    if table.sigma != params.sigma:
+        raise ValueError("influence table was built for a different sigma")
+    _cuda.require_cuda()
+    dev = grid.device_view().device
+    with torch.cuda.device(dev):
+        compute = torch.cuda.current_stream()
+        copy = _COPY_STREAMS.get(str(dev))
+        if copy is None:
+            copy = _COPY_STREAMS[str(dev)] = torch.cuda.Stream()
+        read_done = [None, None]           # per buffer slot: its last read-back
+        pending = None
+        for i, config in enumerate(configs):
+            slot = i & 1
+            if before_frame is not None:
+                before_frame(i)
+            if read_done[slot] is not None:
+                compute.wait_event(read_done[slot])      # slot's previous pixels copied out
+            queued = enqueue_frame(config, grid, table, settings, slot=slot)
+            if queued is None:
+                item = ("background", config)
+            else:
+                buf, plan, plan_ms = queued
+                done = torch.cuda.Event()
+                done.record(compute)
+                pixels = torch.empty((config.height, config.width, 3), dtype=torch.uint8, pin_memory=True)
+                counters = torch.empty(_cuda.N_COUNTERS, dtype=torch.int64, pin_memory=True)
+                with torch.cuda.stream(copy):
+                    copy.wait_event(done)
+                    pixels.copy_(buf.rgb, non_blocking=True)
+                    counters.copy_(buf.counters, non_blocking=True)
+                    read_done[slot] = torch.cuda.Event()
+                    read_done[slot].record(copy)
+                item = ("frame", buf, plan, plan_ms, pixels, counters, read_done[slot])
+            if pending is not None:
+                yield _finish_pending(pending, grid, params)
+            pending = item
+        if pending is not None:
+            yield _finish_pending(pending, grid, params)
+
+
+def _finish_pending(item, grid, params):
+    if item[0] == "background":
+        return _background_frame(item[1], False)
+    _, buf, plan, plan_ms, pixels, counters, ev = item
+    ev.synchronize()
+    return _finish_frame(buf, plan, plan_ms, pixels, counters, grid, params, False)
+
+
+def _finish_frame(buf, plan, plan_ms, pixels, counters, grid, params, debug):
+    cnt = counters.tolist()
     if cnt[_cuda.CNT_ZERO_WEIGHT]:
         raise ValueError(f"zero weight sum while discretizing: influence table inconsistent "
                          f"with sigma={params.sigma}")
