@@ -169,23 +169,20 @@ __global__ void __launch_bounds__(256) k_visibility_mask(HcCascadeRaster c) {
 __device__ int classify_block(const HcCascadeRaster& c, int x0, int y0, int x1, int y1, int lane) {
     const double qx0 = dadd(c.origin_x, dmul((double)x0, c.texel)), qx1 = dadd(c.origin_x, dmul((double)x1, c.texel));
     const double qy0 = dadd(c.origin_y, dmul((double)y0, c.texel)), qy1 = dadd(c.origin_y, dmul((double)y1, c.texel));
+    const double ax = fmax(fabs(qx0), fabs(qx1)), ay = fmax(fabs(qy0), fabs(qy1));
     bool fail_all = false, pass_all = true;
     for (int e0 = 0; e0 < c.n_edges; e0 += 32) {
         const int e = e0 + lane;
         bool fail = false, pass = true;
         if (e < c.n_edges) {
             const double* E = c.edges[e];
-            double lo = INFINITY, hi = -INFINITY, mag = 0.0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const double px = (k & 1) ? qx1 : qx0, py = (k & 2) ? qy1 : qy0;
-                const double cr = dsub(dmul(E[2], dsub(py, E[1])), dmul(E[3], dsub(px, E[0])));
-                lo = fmin(lo, cr);
-                hi = fmax(hi, cr);
-                mag = fmax(mag, dadd(dmul(fabs(E[2]), dadd(fabs(py), fabs(E[1]))),
-                                     dmul(fabs(E[3]), dadd(fabs(px), fabs(E[0])))));
-            }
+            // L(p) = a(p_y) - b(p_x) is separable: its extremes over the box are
+            // min a - max b and max a - min b (corner values, each within the bound)
+            const double a0 = dmul(E[2], dsub(qy0, E[1])), a1 = dmul(E[2], dsub(qy1, E[1]));
+            const double b0 = dmul(E[3], dsub(qx0, E[0])), b1 = dmul(E[3], dsub(qx1, E[0]));
+            const double mag = dadd(dmul(fabs(E[2]), dadd(ay, fabs(E[1]))), dmul(fabs(E[3]), dadd(ax, fabs(E[0]))));
             const double tol = dmul(mag, 0x1p-44);
+            const double lo = dsub(fmin(a0, a1), fmax(b0, b1)), hi = dsub(fmax(a0, a1), fmin(b0, b1));
             fail = dadd(hi, tol) < E[4];
             pass = dsub(lo, tol) >= E[4];
         }
@@ -207,6 +204,7 @@ __global__ void __launch_bounds__(256) k_discretize(const __grid_constant__ Disc
     const bool in_raster = ix < R && iy < R;
     const int64_t o = (int64_t)iy * R + ix;
 
+    // warp 0 classifies the block (a per-warp copy of the classification was measured slower)
     __shared__ int s_cls;
     if (warp == 0) {
         const int cls = classify_block(c, blockIdx.x * 16, blockIdx.y * 16, min((int)blockIdx.x * 16 + 15, R - 1),
