@@ -7,7 +7,8 @@
 // equals the reference's pyramid of the same (float32-representable) raster.
 //
 // Two launches for all K cascades x 2 layers of a frame:
-//   k_mip_tiles : one CTA per 32x32 block of level-0 nodes.  The 33x33 height
+//   k_mip_tiles : one CTA per 32x32 block of level-0 nodes (of both layers of a
+//                 cascade when the jobs come as (terrain, water) pairs).  The 33x33 height
 //                 tile and its valid bytes are staged in shared memory with
 //                 coalesced loads, then levels 0..5 are reduced in shared
 //                 memory (the block is exactly one level-5 node) and written
@@ -33,42 +34,60 @@ struct MipParams {
 
 __device__ __forceinline__ int ceil_shift(int n, int s) { return (n + (1 << s) - 1) >> s; }
 
+// NL = 2: the CTA builds jobs 2z (terrain, with heights_other = the water raster)
+// and 2z+1 (water) of the same cascade together, so the water heights and the
+// valid bytes are read once (9 instead of 14 bytes per texel) and patch bit 1
+// compares the two staged tiles.  NL = 1: one job per CTA (generic jobs).
+template <int NL>
 __global__ void __launch_bounds__(256) k_mip_tiles(const __grid_constant__ MipParams P) {
-    const HcMipJob& J = P.j[blockIdx.z];
-    const int R = J.resolution, n0 = R - 1;
+    const HcMipJob& J0 = P.j[blockIdx.z * NL];
+    const int R = J0.resolution, n0 = R - 1;
     const int tiles_x = (n0 + TILE - 1) / TILE;
     if ((int)blockIdx.x >= tiles_x || (int)blockIdx.y >= tiles_x) return;
     const int bx = blockIdx.x * TILE, by = blockIdx.y * TILE;
 
-    __shared__ float h[TILE + 1][TILE + 2];
+    __shared__ float h[NL][TILE + 1][TILE + 2];
     __shared__ uint8_t vv[TILE + 1][TILE + 4];
-    __shared__ float lv[TILE][TILE + 1];
-    __shared__ float red[2][8];
+    __shared__ float lv[NL][TILE][TILE + 1];
+    __shared__ float red[NL][2][8];
 
     const int tid = threadIdx.x;
-    float vmin = INFINITY, vmax = -INFINITY;
+    float vmin[NL], vmax[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) vmin[l] = INFINITY, vmax[l] = -INFINITY;
     // stage the (TILE+1)^2 texel tile; texel (x, y) is "owned" (counted in the
     // valid range) by the CTA whose node block contains min(x, n0-1)
     for (int e = tid; e < (TILE + 1) * (TILE + 1); e += 256) {
         const int ty = e / (TILE + 1), tx = e % (TILE + 1);
         const int y = by + ty, x = bx + tx;
-        float v = -INFINITY;
+        float v[NL];
+#pragma unroll
+        for (int l = 0; l < NL; ++l) v[l] = -INFINITY;
         uint8_t ok = 0;
         if (x < R && y < R) {
             const int64_t o = (int64_t)y * R + x;
-            v = J.heights[o];
-            ok = J.valid[o] != 0;
+#pragma unroll
+            for (int l = 0; l < NL; ++l) v[l] = P.j[blockIdx.z * NL + l].heights[o];
+            ok = J0.valid[o] != 0;
             // bit 1: this texel differs from the other layer (bitwise: -0.0 vs 0.0 and NaNs
             // count as different, so "same bits" implies every comparison agrees)
-            if (J.heights_other && __float_as_uint(J.heights_other[o]) != __float_as_uint(v)) ok |= 2;
+            if (NL == 2) {
+                if (__float_as_uint(v[NL - 1]) != __float_as_uint(v[0])) ok |= 2;
+            } else if (J0.heights_other && __float_as_uint(J0.heights_other[o]) != __float_as_uint(v[0])) {
+                ok |= 2;
+            }
             const bool own_x = tx < TILE || x == R - 1;
             const bool own_y = ty < TILE || y == R - 1;
             if ((ok & 1) && own_x && own_y) {
-                vmin = fminf(vmin, v);
-                vmax = fmaxf(vmax, v);
+#pragma unroll
+                for (int l = 0; l < NL; ++l) {
+                    vmin[l] = fminf(vmin[l], v[l]);
+                    vmax[l] = fmaxf(vmax[l], v[l]);
+                }
             }
         }
-        h[ty][tx] = v;
+#pragma unroll
+        for (int l = 0; l < NL; ++l) h[l][ty][tx] = v[l];
         vv[ty][tx] = ok;
     }
     __syncthreads();
@@ -77,58 +96,76 @@ __global__ void __launch_bounds__(256) k_mip_tiles(const __grid_constant__ MipPa
     for (int e = tid; e < TILE * TILE; e += 256) {
         const int ty = e / TILE, tx = e % TILE;
         const int y = by + ty, x = bx + tx;
-        float m = -INFINITY;
+        float m[NL];
+#pragma unroll
+        for (int l = 0; l < NL; ++l) m[l] = -INFINITY;
         if (x < n0 && y < n0) {
-            m = fmaxf(fmaxf(h[ty][tx], h[ty][tx + 1]), fmaxf(h[ty + 1][tx], h[ty + 1][tx + 1]));
-            J.mip[(int64_t)y * n0 + x] = m;
-            if (J.patch_ok) {
+#pragma unroll
+            for (int l = 0; l < NL; ++l) {
+                m[l] = fmaxf(fmaxf(h[l][ty][tx], h[l][ty][tx + 1]), fmaxf(h[l][ty + 1][tx], h[l][ty + 1][tx + 1]));
+                P.j[blockIdx.z * NL + l].mip[(int64_t)y * n0 + x] = m[l];
+            }
+            if (J0.patch_ok) {
                 const uint8_t a = vv[ty][tx], b = vv[ty][tx + 1], c = vv[ty + 1][tx], e = vv[ty + 1][tx + 1];
-                J.patch_ok[(int64_t)y * n0 + x] = (uint8_t)((a & b & c & e & 1) | ((a | b | c | e) & 2));
+                J0.patch_ok[(int64_t)y * n0 + x] = (uint8_t)((a & b & c & e & 1) | ((a | b | c | e) & 2));
             }
         }
-        lv[ty][tx] = m;
+#pragma unroll
+        for (int l = 0; l < NL; ++l) lv[l][ty][tx] = m[l];
     }
     __syncthreads();
 
-    // levels 1..5 in place: after level L, lv[y][x] for y, x < TILE >> L holds level L
-    for (int L = 1; L < TILE_LEVELS && L < J.n_levels; ++L) {
+    // levels 1..5 in place: after level L, lv[.][y][x] for y, x < TILE >> L holds level L
+    for (int L = 1; L < TILE_LEVELS && L < J0.n_levels; ++L) {
         const int side = TILE >> L;
-        const int wl = J.level_w[L];
-        float m = -INFINITY;
+        const int wl = J0.level_w[L];
+        float m[NL];
         int y = 0, x = 0;
         if (tid < side * side) {
             y = tid / side;
             x = tid % side;
-            m = fmaxf(fmaxf(lv[2 * y][2 * x], lv[2 * y][2 * x + 1]),
-                      fmaxf(lv[2 * y + 1][2 * x], lv[2 * y + 1][2 * x + 1]));
+#pragma unroll
+            for (int l = 0; l < NL; ++l)
+                m[l] = fmaxf(fmaxf(lv[l][2 * y][2 * x], lv[l][2 * y][2 * x + 1]),
+                             fmaxf(lv[l][2 * y + 1][2 * x], lv[l][2 * y + 1][2 * x + 1]));
         }
         __syncthreads();
         if (tid < side * side) {
-            lv[y][x] = m;
             const int gy = (by >> L) + y, gx = (bx >> L) + x;
-            if (gx < wl && gy < wl) J.mip[J.level_off[L] + (int64_t)gy * wl + gx] = m;
+#pragma unroll
+            for (int l = 0; l < NL; ++l) {
+                lv[l][y][x] = m[l];
+                const HcMipJob& J = P.j[blockIdx.z * NL + l];
+                if (gx < wl && gy < wl) J.mip[J.level_off[L] + (int64_t)gy * wl + gx] = m[l];
+            }
         }
         __syncthreads();
     }
 
-    // CTA partial min/max of valid heights
-    for (int s = 16; s > 0; s >>= 1) {
-        vmin = fminf(vmin, __shfl_xor_sync(0xffffffffu, vmin, s));
-        vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, s));
-    }
-    if ((tid & 31) == 0) {
-        red[0][tid >> 5] = vmin;
-        red[1][tid >> 5] = vmax;
+    // CTA partial min/max of valid heights, per layer
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+        for (int s = 16; s > 0; s >>= 1) {
+            vmin[l] = fminf(vmin[l], __shfl_xor_sync(0xffffffffu, vmin[l], s));
+            vmax[l] = fmaxf(vmax[l], __shfl_xor_sync(0xffffffffu, vmax[l], s));
+        }
+        if ((tid & 31) == 0) {
+            red[l][0][tid >> 5] = vmin[l];
+            red[l][1][tid >> 5] = vmax[l];
+        }
     }
     __syncthreads();
-    if (tid == 0) {
+    if (tid < NL) {
+        const int l = tid;
+        float a = red[l][0][0], b = red[l][1][0];
         for (int w = 1; w < 8; ++w) {
-            vmin = fminf(vmin, red[0][w]);
-            vmax = fmaxf(vmax, red[1][w]);
+            a = fminf(a, red[l][0][w]);
+            b = fmaxf(b, red[l][1][w]);
         }
-        float* pp = P.partial + ((int64_t)blockIdx.z * P.max_tiles + blockIdx.y * tiles_x + blockIdx.x) * 2;
-        pp[0] = vmin;
-        pp[1] = vmax;
+        float* pp =
+            P.partial + ((int64_t)(blockIdx.z * NL + l) * P.max_tiles + blockIdx.y * tiles_x + blockIdx.x) * 2;
+        pp[0] = a;
+        pp[1] = b;
     }
 }
 
@@ -234,8 +271,21 @@ extern "C" int hc_maxmip(const HcMipJob* jobs, int n_jobs, void* workspace, size
                need);
     P.partial = (float*)workspace;
     P.max_tiles = tiles_max * tiles_max;
-    dim3 g(tiles_max, tiles_max, n_jobs);
-    k_mip_tiles<<<g, 256, 0, (cudaStream_t)stream>>>(P);
+    // (terrain, water) job pairs of one cascade share a CTA: job 2c's heights_other is
+    // job 2c+1's heights, same valid bytes and shape, no patch bytes for the water job
+    bool paired = n_jobs % 2 == 0;
+    for (int c = 0; paired && 2 * c < n_jobs; ++c) {
+        const HcMipJob &a = jobs[2 * c], &b = jobs[2 * c + 1];
+        paired = a.heights_other && a.heights_other == b.heights && a.valid == b.valid &&
+                 a.resolution == b.resolution && !b.patch_ok && !b.heights_other;
+    }
+    if (paired) {
+        dim3 g(tiles_max, tiles_max, n_jobs / 2);
+        k_mip_tiles<2><<<g, 256, 0, (cudaStream_t)stream>>>(P);
+    } else {
+        dim3 g(tiles_max, tiles_max, n_jobs);
+        k_mip_tiles<1><<<g, 256, 0, (cudaStream_t)stream>>>(P);
+    }
     k_mip_top<<<n_jobs, 1024, 0, (cudaStream_t)stream>>>(P);
     return cuda_status("hc_maxmip");
 }
