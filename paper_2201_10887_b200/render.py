@@ -136,7 +136,7 @@ class LayerResolve:
 
 
 _BUFFERS: dict = {}
-_COPY_STREAMS: dict = {}       # per device: read-back stream of render_frames
+_SIDE_STREAMS: dict = {}       # per device: render_frames' read-back stream and side compute streams
 
 
 def _frame_buffers(device, K, R, W, H, debug, slot=0):
@@ -215,35 +215,46 @@ def render_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable,
 
 
 def render_frames(configs, grid: AdaptiveGrid, table: InfluenceTable, params: RbfParams,
-                  settings: CascadeSettings = CascadeSettings(), before_frame=None):
+                  settings: CascadeSettings = CascadeSettings(), before_frame=None, depth: int = 3):
     """Render a sequence of frames (a camera path or a batch of views), yielding
     one `Frame` per config, identical to `render_frame`'s.
 
-    Frames alternate between two device buffer sets; frame i's pixels are read
-    back on a copy stream while frame i+1 is planned and computed, so the host
-    planning and the read-back overlap the GPU work.  `before_frame(i)`, if given,
-    is called before frame i is enqueued (e.g. to enqueue an L2 flush)."""
+    Up to `depth` frames are in flight, each with its own device buffer set and
+    compute stream (the caller's and depth-1 side streams): a frame's planning,
+    discretization and mips run while earlier frames' ray casting finishes (whose
+    last long rays leave most SMs idle), and pixels are read back on a copy stream
+    meanwhile.  `before_frame(i)`, if given, is called on frame i's stream before
+    it is enqueued (e.g. to enqueue an L2 flush)."""
+    import collections
     import torch
     if table.sigma != params.sigma:
         raise ValueError("influence table was built for a different sigma")
+    if depth < 1:
+        raise ValueError("depth must be at least 1")
     _cuda.require_cuda()
     dev = grid.device_view().device
     with torch.cuda.device(dev):
-        compute = torch.cuda.current_stream()
-        copy = _COPY_STREAMS.get(str(dev))
-        if copy is None:
-            copy = _COPY_STREAMS[str(dev)] = torch.cuda.Stream()
-        read_done = [None, None]           # per buffer slot: its last read-back
-        pending = None
+        caller = torch.cuda.current_stream()
+        side = _SIDE_STREAMS.setdefault(str(dev), [])
+        while len(side) < depth:           # side[0]: read-back stream, side[1:]: compute streams
+            side.append(torch.cuda.Stream())
+        copy = side[0]
+        streams = [caller] + side[1:depth]
+        for st in streams[1:]:
+            st.wait_stream(caller)         # side streams start after the caller's prior work
+        read_done = [None] * depth         # per buffer slot: its last read-back
+        pending = collections.deque()
         for i, config in enumerate(configs):
-            slot = i & 1
-            if before_frame is not None:
-                before_frame(i)
-            if read_done[slot] is not None:
-                compute.wait_event(read_done[slot])      # slot's previous pixels copied out
-            queued = enqueue_frame(config, grid, table, settings, slot=slot)
+            slot = i % depth
+            compute = streams[slot]
+            with torch.cuda.stream(compute):
+                if before_frame is not None:
+                    before_frame(i)
+                if read_done[slot] is not None:
+                    compute.wait_event(read_done[slot])  # slot's previous pixels copied out
+                queued = enqueue_frame(config, grid, table, settings, slot=slot)
             if queued is None:
-                item = ("background", config)
+                pending.append(("background", config))
             else:
                 buf, plan, plan_ms = queued
                 done = torch.cuda.Event()
@@ -256,12 +267,13 @@ def render_frames(configs, grid: AdaptiveGrid, table: InfluenceTable, params: Rb
                     counters.copy_(buf.counters, non_blocking=True)
                     read_done[slot] = torch.cuda.Event()
                     read_done[slot].record(copy)
-                item = ("frame", buf, plan, plan_ms, pixels, counters, read_done[slot])
-            if pending is not None:
-                yield _finish_pending(pending, grid, params)
-            pending = item
-        if pending is not None:
-            yield _finish_pending(pending, grid, params)
+                pending.append(("frame", buf, plan, plan_ms, pixels, counters, read_done[slot]))
+            if len(pending) >= depth:
+                yield _finish_pending(pending.popleft(), grid, params)
+        for st in streams[1:]:
+            caller.wait_stream(st)         # later work on the caller's stream sees every frame
+        while pending:
+            yield _finish_pending(pending.popleft(), grid, params)
 
 
 def _finish_pending(item, grid, params):
