@@ -12,7 +12,16 @@ for p in (ROOT, os.path.join(ROOT, "oracle"), os.path.join(ROOT, "tests")):
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (CUDA) device")
-    config.addinivalue_line("markers", "slow: long-running case")
+    config.addinivalue_line("markers", "slow: long-running case (run with HC_SLOW=1)")
+
+
+def pytest_collection_modifyitems(config, items):
+    if os.environ.get("HC_SLOW"):
+        return
+    skip = pytest.mark.skip(reason="slow case: set HC_SLOW=1")
+    for item in items:
+        if "slow" in item.keywords:
+            item.add_marker(skip)
 
 
 @pytest.fixture(scope="session")
