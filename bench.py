@@ -189,19 +189,36 @@ def rank_frame_config(cfg, rank, world):
 
 
 def cpu_frames(cfg, g, table, fc, budget_s, max_frames=None):
-    """Oracle (reference CPU port) frames: returns (frames/s, per-frame stats, n)."""
+    """Oracle (reference CPU port) frames: returns (frames/s, per-frame stats, n).
+
+    Every frame is planned by the numpy restatement of the reference planner
+    (oracle/plan_numpy.py) inside the timed frame, then discretized, ray cast and
+    shaded by the float64 C oracle -- no code of the B200 path runs."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import heightcast_oracle as O
+    import plan_numpy as PN
     from paper_2201_10887_b200.rbf import RbfParams
     O.build()
     P = RbfParams(sigma=cfg.sigma)
     st = cfg.settings()
-    O.render_frame(fc, g, table, P, st)              # warm (page-in, thread pool)
+    c = fc.camera
+    cam = PN.CameraView(eye=c.eye, look_dir=c.look_dir, up=c.up, fov_y=c.fov_y, aspect=c.aspect,
+                        near_clip=c.near_clip, far_clip=c.far_clip)
+
+    def frame():
+        tp = time.perf_counter()
+        plan = PN.plan_cascades(cam, g, st.resolution, st.overlap, st.count)
+        plan_ms = (time.perf_counter() - tp) * 1e3
+        _, stats = O.render_frame(fc, g, table, P, st, plan=plan)
+        stats["plan_ms"] = plan_ms
+        return stats
+
+    frame()                                             # warm (page-in, thread pool)
     times, stats = [], None
     t_start = time.perf_counter()
     while True:
         t0 = time.perf_counter()
-        _, stats = O.render_frame(fc, g, table, P, st)
+        stats = frame()
         times.append(time.perf_counter() - t0)
         if time.perf_counter() - t_start >= budget_s or (max_frames and len(times) >= max_frames):
             break
@@ -213,7 +230,12 @@ def run_reference(args, cfg):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    g, table, _ = build_inputs(cfg)
+    # CPU only: the grid from the generator, the influence table from the oracle's
+    # scipy builder (the reference's algorithm), nothing on the GPU
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import heightcast_oracle as O
+    g = cfg.grid()
+    table = O.build_influence_table(g, cfg.sigma)
     fc = rank_frame_config(cfg, 0, 1)
     fps, stats, n, per = cpu_frames(cfg, g, table, fc, budget_s=1e9, max_frames=args.steps)
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
