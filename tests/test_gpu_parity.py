@@ -121,6 +121,17 @@ def _frame_vs_oracle(frame, oracle, cfg, g):
     assert np.array_equal(np.isnan(wd), np.isnan(od["water_depth"]))
     assert np.array_equal(wd[~np.isnan(wd)], od["water_depth"][~np.isnan(wd)])
     assert np.array_equal(frame.pixels, px)
+    # the frame's max mips (built per cascade as (terrain, water) pairs) and valid ranges
+    from paper_2201_10887_b200._engine import key_to_float
+    keys = _np(dbg["vrange_keys"])
+    for k, r in enumerate(r64):
+        for li, (layer, h) in enumerate((("terrain", r.terrain), ("water", r.water))):
+            m = oracle.maxmip(h)
+            assert np.array_equal(_np(dbg["mips"][layer][k]).astype(np.float64)[:m.flat.size], m.flat), (k, layer)
+            vals = h[r.valid]
+            if vals.size:
+                lo, hi = key_to_float(keys[k, li, 0]), key_to_float(keys[k, li, 1])
+                assert (lo, hi) == (float(vals.min()), float(vals.max())), (k, layer)
     return px
 
 
