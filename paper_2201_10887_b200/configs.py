@@ -68,6 +68,6 @@ CONFIGS = {
                       "pond", 11, 300_000, 9, 2.0, 8, 2048, 1920, 1080, (0, 0, 0), (0, 0, 0), views=64,
                       orbit={"cx": 1024.0, "cy": 1024.0, "radius": 1100.0, "z": 350.0, "look_z": 40.0}),
     "C5": BenchConfig("C5", "16384x16384 adaptive quadtree lattice, 8 cascades, 4K in screen strips",
-                      "pond", 13, 600_000, 11, 1.0, 8, 2048, 3840, 2160, (150.0, 100.0, 350.0),
+                      "pond", 13, 2_000_000, 11, 1.0, 8, 2048, 3840, 2160, (150.0, 100.0, 350.0),
                       (1150.0, 1250.0, 50.0)),
 }
