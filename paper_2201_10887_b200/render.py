@@ -145,6 +145,9 @@ def _frame_buffers(device, K, R, W, H, debug, slot=0):
     buf = _BUFFERS.get(key)
     if buf is None:
         if len(_BUFFERS) > 8:
+            # buffers may still be in use by queued frames (render_frames runs them
+            # on side streams): let the device finish before releasing them
+            torch.cuda.synchronize()
             _BUFFERS.clear()
         buf = _engine.FrameBuffers(torch.device(device), K, R, W, H, debug=debug)
         _BUFFERS[key] = buf
