@@ -238,6 +238,7 @@ def render_frames(configs, grid: AdaptiveGrid, table: InfluenceTable, params: Rb
     dev = grid.device_view().device
     with torch.cuda.device(dev):
         caller = torch.cuda.current_stream()
+        grid.device_view().influence(table)    # upload / build records now, before the side streams fork
         side = _SIDE_STREAMS.setdefault(str(dev), [])
         while len(side) < depth:           # side[0]: read-back stream, side[1:]: compute streams
             side.append(torch.cuda.Stream())
