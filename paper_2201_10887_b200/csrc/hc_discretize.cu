@@ -139,10 +139,21 @@ __device__ __forceinline__ bool texel_visible(const HcCascadeRaster& c, double p
     return in;
 }
 
-// grid.py:200-210
+// 1 / m when m is a power of two in the normal range (then x / m and x * (1/m) are
+// the same correctly rounded value of the same real number), else 0
+__device__ __forceinline__ double exact_reciprocal(double m) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(m);
+    const unsigned long long e = (b >> 52) & 0x7ffu;
+    if ((b & 0x800fffffffffffffull) != 0ull || e < 1u || e > 2045u) return 0.0;
+    return __longlong_as_double((long long)((2046u - e) << 52));
+}
+
+// grid.py:200-210 (the division is a multiplication when min_cell is a power of two)
 __device__ __forceinline__ int containing_cell(const HcGrid& g, double px, double py) {
-    const double fx = floor(ddiv(dsub(px, g.xmin), g.min_cell));
-    const double fy = floor(ddiv(dsub(py, g.ymin), g.min_cell));
+    const double inv = exact_reciprocal(g.min_cell);
+    const double qx = dsub(px, g.xmin), qy = dsub(py, g.ymin);
+    const double fx = floor(inv != 0.0 ? dmul(qx, inv) : ddiv(qx, g.min_cell));
+    const double fy = floor(inv != 0.0 ? dmul(qy, inv) : ddiv(qy, g.min_cell));
     if (!(fx >= 0.0 && fy >= 0.0 && fx < (double)g.ntx && fy < (double)g.nty)) return -1;
     return g.tile_index[(int64_t)fy * g.ntx + (int64_t)fx];
 }

@@ -218,11 +218,11 @@ def render_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable,
 
 
 def render_frames(configs, grid: AdaptiveGrid, table: InfluenceTable, params: RbfParams,
-                  settings: CascadeSettings = CascadeSettings(), before_frame=None, depth: int = 3):
+                  settings: CascadeSettings = CascadeSettings(), before_frame=None, depth: int = 4):
     """Render a sequence of frames (a camera path or a batch of views), yielding
     one `Frame` per config, identical to `render_frame`'s.
 
-    Up to `depth` frames are in flight, each with its own device buffer set and
+    Up to `depth` (default 4) frames are in flight, each with its own device buffer set and
     compute stream (the caller's and depth-1 side streams): a frame's planning,
     discretization and mips run while earlier frames' ray casting finishes (whose
     last long rays leave most SMs idle), and pixels are read back on a copy stream

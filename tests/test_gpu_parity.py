@@ -93,6 +93,36 @@ def test_discretize_demo_matches_oracle(cuda, oracle):
         assert np.all(_np(r.water) >= _np(r.terrain))
 
 
+def test_discretize_non_power_of_two_min_cell(cuda, oracle):
+    """min_cell = 3 x the demo's: the cell lookup takes the IEEE-division path."""
+    import dataclasses
+    from paper_2201_10887_b200 import AdaptiveGrid, cascade, discretize_cascade
+    from paper_2201_10887_b200.cascade import CameraView
+    from paper_2201_10887_b200.grid import Rect
+    from paper_2201_10887_b200.rbf import RbfParams
+    import heightcast_oracle as O
+    sc, g0, _, cfg, st = demo_setup()
+    d = g0.domain
+    g = AdaptiveGrid(Rect(3 * d.xmin, 3 * d.ymin, 3 * d.xmax, 3 * d.ymax), 3 * g0.min_cell_size,
+                     3 * g0.centers, 3 * g0.sizes, g0.terrain, g0.water_depth)
+    t = O.build_influence_table(g, sc.sigma)
+    c = cfg.camera
+    cam = dataclasses.replace(c, eye=(3 * c.eye[0], 3 * c.eye[1], c.eye[2]),
+                              look_dir=(3 * c.look_dir[0], 3 * c.look_dir[1], c.look_dir[2]))
+    assert isinstance(cam, CameraView)
+    _, _, lays = cascade.plan_cascades(cam, g, st.resolution, st.overlap, st.count)
+    n = 0
+    for L in (l for l in lays if l is not None):
+        r = discretize_cascade(L, g, t, RbfParams(sigma=sc.sigma))
+        o = oracle.discretize(L, g, t, sc.sigma)
+        valid = _np(r.valid)
+        assert np.array_equal(valid, o.valid)
+        _check_heights(_np(r.terrain), o.terrain, valid, "terrain")
+        _check_heights(_np(r.water), o.water, valid, "water")
+        n += int(valid.sum())
+    assert n > 0
+
+
 def _frame_vs_oracle(frame, oracle, cfg, g):
     """Feed the oracle the GPU's own rasters; every raycast output must match bitwise."""
     dbg = frame.debug
