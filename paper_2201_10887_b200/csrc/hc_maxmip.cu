@@ -19,7 +19,10 @@
 //                 nodes at R=2048) and folds the partial min/max into the
 //                 job's valid range.  No atomics, no init pass: deterministic.
 // HBM traffic per job ~ 4*(R^2 + nodes) + R^2 bytes (valid), each byte once.
+#include <string.h>
+
 #include "hc_internal.cuh"
+#include "hc_order.cuh"
 
 namespace hc {
 
@@ -30,6 +33,9 @@ struct MipParams {
     HcMipJob j[2 * HC_MAX_CASCADES];
     float* partial;                 // [n_jobs][max_tiles][2]
     int32_t max_tiles;
+    int32_t tiles_grid;             // k_mip_tiles: mip CTAs per grid row (columns past it count the order)
+    int32_t n_jobs;                 // k_mip_top: CTAs past n_jobs scatter the order
+    OrderJob ord;                   // tile-queue order of the frame's k_render (n_tiles 0: none)
 };
 
 __device__ __forceinline__ int ceil_shift(int n, int s) { return (n + (1 << s) - 1) >> s; }
@@ -40,6 +46,12 @@ __device__ __forceinline__ int ceil_shift(int n, int s) { return (n + (1 << s) -
 // compares the two staged tiles.  NL = 1: one job per CTA (generic jobs).
 template <int NL>
 __global__ void __launch_bounds__(256) k_mip_tiles(const __grid_constant__ MipParams P) {
+    if ((int)blockIdx.x >= P.tiles_grid) {       // tile-queue order: one histogram chunk per CTA
+        const int chunk = ((int)blockIdx.x - P.tiles_grid) * (int)gridDim.y + (int)blockIdx.y;
+        if (blockIdx.z == 0 && chunk < order_chunks(P.ord.n_tiles))
+            order_count_chunk<256>(P.ord.cost, P.ord.order, P.ord.n_tiles, chunk);
+        return;
+    }
     const HcMipJob& J0 = P.j[blockIdx.z * NL];
     const int R = J0.resolution, n0 = R - 1;
     const int tiles_x = (n0 + TILE - 1) / TILE;
@@ -170,6 +182,10 @@ __global__ void __launch_bounds__(256) k_mip_tiles(const __grid_constant__ MipPa
 }
 
 __global__ void __launch_bounds__(1024) k_mip_top(const __grid_constant__ MipParams P) {
+    if ((int)blockIdx.x >= P.n_jobs) {           // tile-queue order: ranks of one chunk
+        order_scatter_chunk(P.ord.cost, P.ord.order, P.ord.n_tiles, P.ord.counter, (int)blockIdx.x - P.n_jobs);
+        return;
+    }
     const HcMipJob& J = P.j[blockIdx.x];
     const int tid = threadIdx.x;
     const int tiles_x = (J.resolution - 1 + TILE - 1) / TILE;
@@ -244,6 +260,11 @@ extern "C" size_t hc_maxmip_workspace_bytes(int n_jobs, int max_resolution) {
 
 extern "C" int hc_maxmip(const HcMipJob* jobs, int n_jobs, void* workspace, size_t workspace_bytes,
                          hc_stream_t stream) {
+    return hc::maxmip_launch(jobs, n_jobs, workspace, workspace_bytes, nullptr, (cudaStream_t)stream);
+}
+
+int hc::maxmip_launch(const HcMipJob* jobs, int n_jobs, void* workspace, size_t workspace_bytes,
+                      const OrderJob* ord, cudaStream_t stream) {
     HC_REQUIRE(jobs, "hc_maxmip: null jobs");
     HC_REQUIRE(n_jobs >= 0 && n_jobs <= 2 * HC_MAX_CASCADES, "hc_maxmip: %d jobs (max %d)", n_jobs,
                2 * HC_MAX_CASCADES);
@@ -279,13 +300,23 @@ extern "C" int hc_maxmip(const HcMipJob* jobs, int n_jobs, void* workspace, size
         paired = a.heights_other && a.heights_other == b.heights && a.valid == b.valid &&
                  a.resolution == b.resolution && !b.patch_ok && !b.heights_other;
     }
-    if (paired) {
-        dim3 g(tiles_max, tiles_max, n_jobs / 2);
-        k_mip_tiles<2><<<g, 256, 0, (cudaStream_t)stream>>>(P);
-    } else {
-        dim3 g(tiles_max, tiles_max, n_jobs);
-        k_mip_tiles<1><<<g, 256, 0, (cudaStream_t)stream>>>(P);
+    P.tiles_grid = tiles_max;
+    P.n_jobs = n_jobs;
+    memset(&P.ord, 0, sizeof(P.ord));
+    int nc = 0;
+    if (ord && ord->n_tiles > 0) {
+        HC_REQUIRE(ord->cost && ord->order && ord->counter, "hc_maxmip: order job with null pointers");
+        P.ord = *ord;
+        nc = order_chunks(ord->n_tiles);
     }
-    k_mip_top<<<n_jobs, 1024, 0, (cudaStream_t)stream>>>(P);
+    const int order_cols = (nc + tiles_max - 1) / tiles_max;
+    if (paired) {
+        dim3 g(tiles_max + order_cols, tiles_max, n_jobs / 2);
+        k_mip_tiles<2><<<g, 256, 0, stream>>>(P);
+    } else {
+        dim3 g(tiles_max + order_cols, tiles_max, n_jobs);
+        k_mip_tiles<1><<<g, 256, 0, stream>>>(P);
+    }
+    k_mip_top<<<n_jobs + nc, 1024, 0, stream>>>(P);
     return cuda_status("hc_maxmip");
 }

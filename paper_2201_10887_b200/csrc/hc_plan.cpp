@@ -658,6 +658,8 @@ extern "C" int hc_plan_cascades(const HcCamera* cam, const HcDomain* dom, int re
 
 #include <cuda_runtime.h>
 
+#include "hc_launch.h"
+
 namespace {
 
 void level_shape(int R, int64_t* off, int32_t* w, int* n) {
@@ -806,10 +808,13 @@ extern "C" int hc_frame_launch(const HcPlan* plan, const HcCamera* cam, const Hc
     int rc = hc_discretize(cr, K, grid, (float)(dom->h_lo - 1.0), buf->counters, stream);
     if (rc) return rc;
     rec(1);
-    rc = hc_maxmip(jobs, 2 * K, buf->mip_ws, buf->mip_ws_bytes, stream);
+    // the render's tile-queue order is computed inside the two max-mip launches
+    hc::OrderJob ord{A.tile_cost, A.tile_order, A.tile_counter,
+                     A.tile_order ? (int32_t)hc_render_tiles(A.x0, A.y0, A.x1, A.y1) : 0};
+    rc = hc::maxmip_launch(jobs, 2 * K, buf->mip_ws, buf->mip_ws_bytes, &ord, s);
     if (rc) return rc;
     rec(2);
-    rc = hc_render(&A, stream);
+    rc = hc::render_launch(&A, A.tile_order != nullptr, s);
     if (rc) return rc;
     rec(3);
     return HC_OK;
