@@ -372,6 +372,10 @@ int hc_frame_launch(const HcPlan *plan, const HcCamera *cam, const HcDomain *dom
 /* Self-test of the hoisted float64 division used by the traversal: counts operand
  * pairs (n pseudo-random + structured) where it differs from IEEE a / b. */
 int hc_selftest_division(uint64_t n, uint64_t seed, uint64_t *mismatches, hc_stream_t stream);
+/* Self-test of the ray/patch test's exact early rejections: counts generated cases
+ * where it differs from the reference's sequence alone (counts[0]), hits
+ * (counts[1]) and misses starting below the patch (counts[2]); device uint64[3]. */
+int hc_selftest_patch(uint64_t n, uint64_t seed, uint64_t *counts, hc_stream_t stream);
 
 #ifdef __cplusplus
 }

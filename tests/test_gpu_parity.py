@@ -251,6 +251,20 @@ def test_benchmark_config_frame_parity(cuda, oracle, name, size, view):
     print(f"{name}: max |dh| = {worst:.3e} m, rays_hit = {fr.rays_hit}")
 
 
+def test_patch_early_rejection_selftest(cuda):
+    """The ray/patch test with its exact early rejections equals the reference's
+    sequence bit for bit on 2^26 generated cases (roots at the segment ends,
+    near-tangent rays, rays starting under the patch)."""
+    import torch
+    from paper_2201_10887_b200 import _cuda
+    cnt = torch.zeros(3, dtype=torch.int64, device=cuda)
+    _cuda.check(_cuda.lib().hc_selftest_patch(1 << 26, 77, cnt.data_ptr(), _cuda.stream_ptr()), "selftest")
+    bad, hits, below = (int(x) for x in cnt.tolist())
+    print(f"patch selftest: {bad} mismatches, {hits} hits, {below} misses from below")
+    assert hits > 1000 and below > 1000
+    assert bad == 0
+
+
 def test_division_selftest(cuda):
     """The traversal's hoisted float64 division equals IEEE a / b on 2^28 operand pairs."""
     import torch
