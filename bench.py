@@ -352,9 +352,10 @@ def main():
 
     # ---- e2e through the public API, host wall clock: every frame planned on the host,
     # its descriptors passed to the GPU, its pixels read back into pinned host memory.
-    # Views: render_frames (read-back of frame i overlaps frame i+1), an L2 flush
-    # enqueued before every frame.  Strips: render_strip + image gather per step.
-    if not strips:
+    # Views (and strips on one GPU, where the strip is the frame): render_frames
+    # (frames overlap, read-back on a copy stream), an L2 flush enqueued before
+    # every frame.  Strips on N > 1 GPUs: render_strip + image gather per step.
+    if not strips or ws == 1:
         from paper_2201_10887_b200 import render_frames
         seq = [views[i % len(views)] for i in range(args.steps)]
         for _ in render_frames(seq[:4] * 4, g, table, P, st):      # every buffer set, pinned blocks
