@@ -265,6 +265,52 @@ def test_patch_early_rejection_selftest(cuda):
     assert bad == 0
 
 
+def _random_poses():
+    """Camera poses over the C2 grid (domain [0, 2048]^2, heights ~12-100 m) that
+    stress the traversal's exact shortcuts: axis-aligned and integer-coordinate
+    eyes (rays through node corners, dx = 0 / dy = 0 columns), a horizontal view
+    axis (dz = 0 rows), grazing eyes just above the terrain, an eye below the
+    terrain, eyes outside the domain, plus seeded random poses."""
+    rng = np.random.default_rng(2201)
+    poses = [
+        ((1024.0, 1024.0, 400.0), (0.0, 0.0, -1.0), (0.0, 1.0, 0.0), 50.0),     # straight down
+        ((512.0, 512.0, 60.0), (1.0, 0.0, 0.0), (0.0, 0.0, 1.0), 60.0),         # horizontal, +x
+        ((1500.0, 300.0, 45.0), (0.0, 1.0, 0.0), (0.0, 0.0, 1.0), 70.0),        # horizontal, +y
+        ((256.0, 256.0, 150.0), (1.0, 1.0, -0.25), (0.0, 0.0, 1.0), 55.0),      # diagonal through corners
+        ((-200.0, 1024.0, 90.0), (1.0, 0.0, -0.05), (0.0, 0.0, 1.0), 40.0),     # outside, grazing in
+        ((1024.0, 1024.0, 20.0), (0.3, -1.0, 0.0), (0.0, 0.0, 1.0), 80.0),      # low, near the terrain
+        ((900.0, 1100.0, 5.0), (1.0, 0.2, 0.1), (0.0, 0.0, 1.0), 60.0),         # below most of the terrain
+        ((2300.0, 2300.0, 800.0), (-1.0, -1.0, -0.8), (0.0, 0.0, 1.0), 35.0),   # far outside, high
+    ]
+    for _ in range(8):
+        eye = (float(rng.uniform(-300, 2350)), float(rng.uniform(-300, 2350)), float(rng.uniform(15, 600)))
+        tgt = (float(rng.uniform(200, 1850)), float(rng.uniform(200, 1850)), float(rng.uniform(0, 80)))
+        look = tuple(b - a for a, b in zip(eye, tgt))
+        poses.append((eye, look, (0.0, 0.0, 1.0), float(rng.uniform(30, 90))))
+    return poses
+
+
+@pytest.mark.parametrize("i", range(16))
+def test_random_pose_frame_parity(cuda, oracle, i):
+    """Bit-exact ray casting on the GPU's rasters for 16 poses (see _random_poses),
+    with 1..6 cascades of 256^2 or 512^2 at 320x200."""
+    from paper_2201_10887_b200 import render_frame
+    from paper_2201_10887_b200.cascade import CameraView
+    from paper_2201_10887_b200.rbf import RbfParams
+    from paper_2201_10887_b200.render import CascadeSettings, FrameConfig
+    cfg, g, t, _ = _config_inputs("C2")
+    eye, look, up, fov = _random_poses()[i]
+    W, H = 320, 200
+    cam = CameraView(eye=eye, look_dir=look, up=up, fov_y=fov, aspect=W / H, near_clip=1.0, far_clip=6000.0)
+    st = CascadeSettings(resolution=(256, 512)[i % 2], count=1 + i % 6)
+    fc = FrameConfig(width=W, height=H, camera=cam)
+    fr = render_frame(fc, g, t, RbfParams(sigma=cfg.sigma), st, debug=True)
+    if not fr.visible:
+        pytest.skip("nothing visible from this pose")
+    _frame_vs_oracle(fr, oracle, fc, g)
+    print(f"pose {i}: K={st.count} R={st.resolution} rays_hit={fr.rays_hit}")
+
+
 def test_division_selftest(cuda):
     """The traversal's hoisted float64 division equals IEEE a / b on 2^28 operand pairs."""
     import torch
