@@ -418,14 +418,24 @@ def main():
         k["frac"] = k["achieved"] / k["peak"]
     dominant = max(kernels, key=lambda n: kernels[n]["ms"])
     traffic = None
+    prof = {}
     try:
         with open(PROFILE_SUMMARY) as fh:
-            traffic = json.load(fh).get(cfg.name, {}).get(dominant)
+            prof = json.load(fh).get(cfg.name, {})
+        traffic = prof.get(dominant)
     except (OSError, ValueError):
         pass
+    # the issue roofline from the committed ncu capture of this config (fraction of
+    # cycles an instruction issued): where the byte/ex2 roofline is far, this says
+    # whether the kernel is instruction-bound or stalled on latency
+    for name, k in kernels.items():
+        ia = prof.get("issue_active", {}).get(name)
+        if ia is not None:
+            k["ncu_issue_active"] = ia
     d = kernels[dominant]
     roofline = {"kernel": dominant, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
                 "unit": d["unit"], "frac": d["frac"], "traffic": traffic,
+                "ncu_issue_active": d.get("ncu_issue_active"),
                 "peak_source": f"{peak_kind} MEASURED_PEAKS.json" if d["bound"] == "hbm"
                 else f"148 SMs x 16 ex2/clk x {sm_max:.0f} MHz ({peak_kind} sm_max_mhz)"}
 

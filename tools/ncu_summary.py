@@ -89,10 +89,16 @@ def summarise(rep, tag, config):
     path = os.path.join(PROF, "ncu_traffic.json")
     data = json.load(open(path)) if os.path.exists(path) else {}
     per = defaultdict(float)
+    issue = defaultdict(lambda: [0.0, 0.0])     # key -> [sum(duration * issue active), sum(duration)]
     for short, r in kernels:
         key = KERNEL_KEY.get(short.replace("void ", "").split("<")[0].strip())
         if key is None:
             continue
+        dur = to_float(r[col["gpu__time_duration.sum"]]) or 0.0
+        ia = to_float(r[col["smsp__issue_active.avg.pct_of_peak_sustained_active"]])
+        if ia is not None:
+            issue[key][0] += dur * ia / 100.0
+            issue[key][1] += dur
         rd = to_float(r[col["dram__bytes_read.sum"]])
         wr = to_float(r[col["dram__bytes_write.sum"]])
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -101,6 +107,9 @@ def summarise(rep, tag, config):
         per[key] += rd + wr
     data.setdefault(config, {}).update({k: v for k, v in per.items()})
     data[config]["_source"] = os.path.basename(rep)
+    # fraction of cycles the SM sub-partitions issued an instruction (duration-weighted
+    # over the kernels of one ABI call): the issue roofline of latency-bound kernels
+    data[config]["issue_active"] = {k: round(a / d, 4) for k, (a, d) in issue.items() if d > 0}
     with open(path, "w") as fh:
         json.dump(data, fh, indent=1, sort_keys=True)
     print("wrote", os.path.join(PROF, f"{tag}.md"), dict(per))
