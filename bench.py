@@ -295,7 +295,9 @@ def main():
     torch.cuda.synchronize()
     prep["upload_s"] = round(time.perf_counter() - t_up, 3)
 
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    # L2 flush: 256 MiB (> 126 MB L2) written with 4-byte elements (the fill kernel
+    # runs at full HBM bandwidth; a byte-typed fill reaches about half of it)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)
 
     def barrier():
         if ws > 1:

@@ -27,7 +27,7 @@ def main():
     dev = torch.device("cuda", 0)
     g.device_view(dev).influence(table)
     fc = cfg.frame_config(0)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = torch.empty(64 << 20, dtype=torch.int32, device=dev)
     seq = [fc] * a.frames
     for _ in R.render_frames(seq[:8], g, table, P, st):
         pass
