@@ -74,6 +74,32 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def l2_bandwidth_gbs(dev):
+    """L2 read bandwidth: one launch of hc_bench_l2_read streaming a 32 MiB buffer
+    (L2-resident, 126 MB L2) 64 times, best of 5, CUDA events.  The secondary
+    roofline of the max-mip builder, whose inputs the discretization has just
+    written (SURVEY.md §8 d)."""
+    import torch
+    from paper_2201_10887_b200 import _cuda
+    n = 32 << 20
+    passes = 64
+    buf = torch.ones(n // 4, dtype=torch.float32, device=dev)
+    sink = torch.zeros(1, dtype=torch.float32, device=dev)
+    lib = _cuda.lib()
+    run = lambda: _cuda.check(lib.hc_bench_l2_read(buf.data_ptr(), n, passes, sink.data_ptr(),
+                                                    _cuda.stream_ptr()), "hc_bench_l2_read")
+    run()
+    best = float("inf")
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run()
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    return passes * n / (best * 1e-3) / 1e9
+
+
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled during the timed region.
 
@@ -418,6 +444,10 @@ def main():
     }
     for k in kernels.values():
         k["frac"] = k["achieved"] / k["peak"]
+    l2_gbs = l2_bandwidth_gbs(dev)
+    kernels["hc_maxmip"]["l2_peak_gbs"] = l2_gbs
+    kernels["hc_maxmip"]["frac_l2"] = kernels["hc_maxmip"]["achieved"] / l2_gbs
+    work["pairs_per_valid_texel"] = work["pairs"] / max(work["valid_texels"], 1)
     dominant = max(kernels, key=lambda n: kernels[n]["ms"])
     traffic = None
     prof = {}
