@@ -18,6 +18,8 @@
  *   hco_discretize        discretize.py:52-108 (sentinel, valid, both layers)
  *   hco_maxmip            raycast.py:61-88 (4-corner max, 2x2 max, -inf pad)
  *   hco_traverse_batch    _kernels.py:26-232 (slab clip, max-mip walk, patch)
+ *   hco_dda_batch         SPEC.md:316-334,473 brute-force DDA patch walk (the
+ *                         acceptance oracle of the max-mip traversal)
  *   hco_ray_dirs          render.py:100-110
  *   hco_resolve_layer     render.py:149-186 (nearest-first + overlap blend)
  *   hco_shade             render.py:189-341 (gradients, blended fields,
@@ -349,6 +351,82 @@ void hco_traverse_batch(const double *heights, const uint8_t *valid, const doubl
         const hco_hit h = traverse_one(heights, valid, mflat, moff, mw, nlev, n0, rx[i], ry[i],
                                        rz[i], dx[i], dy[i], dz[i], hmin, hmax,
                                        out_visits ? out_visits + i : 0);
+        out_hit[i] = (uint8_t)h.hit;
+        out_t[i] = h.t;
+        out_ix[i] = h.ix;
+        out_iy[i] = h.iy;
+        out_u[i] = h.u;
+        out_v[i] = h.v;
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* brute-force DDA patch walk (the acceptance oracle of
+ * traverse_cascade): the same slab clip and patch test as traverse_one, but every
+ * cell along the ray's 2D walk is tested in order -- no pyramid, no skipping.   */
+
+static hco_hit dda_one(const double *H, const uint8_t *V, int64_t n0, double rx, double ry, double rz,
+                       double dx, double dy, double dz, double hmin, double hmax, int32_t *cells)
+{
+    const hco_hit miss = {0, 0.0, -1, -1, 0.0, 0.0};
+    const int64_t R = n0 + 1;
+    double t0 = 0.0, t1 = HCO_FAR;
+    const double fn0 = (double)n0;
+    const double org[3] = {rx, ry, rz}, dir[3] = {dx, dy, dz};
+    const double lo[3] = {0.0, 0.0, hmin}, hi[3] = {fn0, fn0, hmax};
+    for (int ax = 0; ax < 3; ++ax) {
+        if (dir[ax] != 0.0) {
+            double ta = (lo[ax] - org[ax]) / dir[ax];
+            double tb = (hi[ax] - org[ax]) / dir[ax];
+            if (ta > tb) { const double s = ta; ta = tb; tb = s; }
+            if (ta > t0) t0 = ta;
+            if (tb < t1) t1 = tb;
+        } else if (org[ax] < lo[ax] || org[ax] > hi[ax]) {
+            return miss;
+        }
+    }
+    if (t0 > t1) return miss;
+    int64_t cx = (int64_t)floor(rx + (t0 * dx));
+    int64_t cy = (int64_t)floor(ry + (t0 * dy));
+    if (cx < 0) cx = 0; else if (cx > n0 - 1) cx = n0 - 1;
+    if (cy < 0) cy = 0; else if (cy > n0 - 1) cy = n0 - 1;
+    double t = t0;
+    for (;;) {
+        if (cells) *cells += 1;
+        double tx = HCO_FAR, ty = HCO_FAR;
+        if (dx > 0.0) tx = ((double)(cx + 1) - rx) / dx; else if (dx < 0.0) tx = ((double)cx - rx) / dx;
+        if (dy > 0.0) ty = ((double)(cy + 1) - ry) / dy; else if (dy < 0.0) ty = ((double)cy - ry) / dy;
+        const double t_wall = (tx <= ty) ? tx : ty;
+        const double seg_end = (t_wall <= t1) ? t_wall : t1;
+        const int64_t k = cy * R + cx;
+        if (V[k] && V[k + 1] && V[k + R] && V[k + R + 1]) {
+            double tau, u, v;
+            const double u0 = (rx + (t * dx)) - (double)cx;
+            const double v0 = (ry + (t * dy)) - (double)cy;
+            const double z0 = rz + (t * dz);
+            if (patch_roots(H[k], H[k + 1], H[k + R], H[k + R + 1], u0, v0, dx, dy, z0, dz, seg_end - t,
+                            &tau, &u, &v)) {
+                const hco_hit h = {1, t + tau, (int32_t)cx, (int32_t)cy, u, v};
+                return h;
+            }
+        }
+        if (t_wall > t1) return miss;
+        if (tx <= ty) { t = tx; cx += (dx > 0.0) ? 1 : -1; }
+        else { t = ty; cy += (dy > 0.0) ? 1 : -1; }
+        if (cx < 0 || cx > n0 - 1 || cy < 0 || cy > n0 - 1 || t > t1) return miss;
+    }
+}
+
+void hco_dda_batch(const double *heights, const uint8_t *valid, int64_t n0, const double *rx, const double *ry,
+                   const double *rz, const double *dx, const double *dy, const double *dz, int64_t n,
+                   double hmin, double hmax, uint8_t *out_hit, double *out_t, int32_t *out_ix,
+                   int32_t *out_iy, double *out_u, double *out_v, int32_t *out_cells /* may be NULL */)
+{
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int64_t i = 0; i < n; ++i) {
+        if (out_cells) out_cells[i] = 0;
+        const hco_hit h = dda_one(heights, valid, n0, rx[i], ry[i], rz[i], dx[i], dy[i], dz[i], hmin, hmax,
+                                  out_cells ? out_cells + i : 0);
         out_hit[i] = (uint8_t)h.hit;
         out_t[i] = h.t;
         out_ix[i] = h.ix;

@@ -138,6 +138,40 @@ def test_oracle_traversal_matches_reference_kernel(oracle):
     assert n_rays >= 10_000
 
 
+def _dda_agreement(got, want, case):
+    """same hit/miss verdict, t within 1e-9, hit residual < 1e-6 m (and the
+    same patch) between a traversal result and the brute-force DDA walk."""
+    hit_g, t_g, ix_g, iy_g, u_g, v_g = (np.asarray(a) for a in got[:6])
+    hit_w, t_w, ix_w, iy_w = want[:4]
+    assert np.array_equal(hit_g.astype(bool), hit_w.astype(bool)), case["name"]
+    m = hit_w.astype(bool)
+    assert np.array_equal(ix_g[m], ix_w[m]) and np.array_equal(iy_g[m], iy_w[m]), case["name"]
+    assert np.all(np.abs(t_g[m] - t_w[m]) <= 1e-9 * np.maximum(1.0, np.abs(t_w[m]))), case["name"]
+    rx, ry, rz, dx, dy, dz = (np.broadcast_to(np.asarray(a, dtype=np.float64), hit_w.shape) for a in case["rays"])
+    h = np.asarray(case["heights"], dtype=np.float64)
+    ix, iy, u, v = ix_g[m], iy_g[m], u_g[m], v_g[m]
+    surf = ((h[iy, ix] * (1 - u) + h[iy, ix + 1] * u) * (1 - v) + (h[iy + 1, ix] * (1 - u) + h[iy + 1, ix + 1] * u) * v)
+    resid = np.abs(rz[m] + t_g[m] * dz[m] - surf)
+    assert np.all(resid < 1e-6), (case["name"], float(resid.max()) if resid.size else 0.0)
+    return int(m.sum())
+
+
+def test_oracle_traversal_equals_dda_walk(oracle):
+    """SPEC.md:473 [PRIMARY]: the max-mip traversal equals brute-force sequential patch
+    testing along the ray's DDA cell walk on >= 1e4 random rays over >= 20 rasters."""
+    n_rays = n_hits = 0
+    for case in gi.traversal_cases():
+        h, valid = case["heights"], case["valid"]
+        vals = h[valid.astype(bool)]
+        lo, hi = float(vals.min()), float(vals.max())
+        mip = oracle.maxmip(h)
+        got = oracle.traverse_batch(h, valid, mip, *case["rays"], lo, hi)
+        want = oracle.dda_batch(h, valid, *case["rays"], lo, hi)
+        n_hits += _dda_agreement(got, want, case)
+        n_rays += len(got[0])
+    assert n_rays >= 10_000 and n_hits >= 1000
+
+
 def test_oracle_eq2_matches_reference(oracle):
     data = npz("rbf_points.npz")
     worst = 0.0
