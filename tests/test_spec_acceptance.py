@@ -187,3 +187,38 @@ def test_approximate_equals_exhaustive_sum(cuda):
                     assert abs(got - (ter + dep)) <= 1e-12 * abs(ter + dep), (case["name"], p, got, ter + dep)
             n_pts += 1
     assert n_pts >= 2000
+
+
+@pytest.mark.gpu
+def test_blend_endpoints_and_convexity(cuda):
+    """blended depths are convex combinations of the two cascades'
+    hits and the blend endpoints reproduce single-cascade hits exactly (w = 0: the
+    near cascade's t; w = 1: the far one's), on the C2 frame and one orbit pose."""
+    from paper_2201_10887_b200 import build_influence_table, render_frame
+    from paper_2201_10887_b200.configs import CONFIGS
+    from paper_2201_10887_b200.rbf import RbfParams
+    cfg = CONFIGS["C2"]
+    g = cfg.grid()
+    t = build_influence_table(g, cfg.sigma)
+    n_blend = 0
+    for view in (0, 1):
+        fc = cfg.frame_config(view)
+        fr = render_frame(fc, g, t, RbfParams(cfg.sigma), cfg.settings(), debug=True)
+        for layer in ("terrain", "water"):
+            L = fr.debug[layer]
+            hit = L.hit.cpu().numpy()
+            far = L.far.cpu().numpy()
+            w = L.w.cpu().numpy()
+            tt = L.t.cpu().numpy()
+            t0 = L.raw_slots["t"][0].cpu().numpy()
+            t1 = L.raw_slots["t"][1].cpu().numpy()
+            b = hit & (far >= 0)
+            assert np.all((w[b] >= 0.0) & (w[b] <= 1.0))
+            lo, hi = np.minimum(t0[b], t1[b]), np.maximum(t0[b], t1[b])
+            assert np.all((tt[b] >= lo * (1 - 1e-15)) & (tt[b] <= hi * (1 + 1e-15)))
+            e0, e1 = b & (w == 0.0), b & (w == 1.0)
+            assert np.array_equal(tt[e0], t0[e0]) and np.array_equal(tt[e1], t1[e1])
+            single = hit & (far < 0)
+            assert np.array_equal(tt[single], t0[single])
+            n_blend += int(b.sum())
+    assert n_blend > 1000
