@@ -44,6 +44,18 @@ def child(cfg_name, frames, selftest):
         d.append(buf.ev[0].elapsed_time(buf.ev[1]))
         m.append(buf.ev[1].elapsed_time(buf.ev[4]))
         r.append(buf.ev[4].elapsed_time(buf.ev[2]))
+    # pipelined sequence (the e2e path): 200 frames through render_frames, L2 flush per frame
+    import time
+    from paper_2201_10887_b200 import render_frames
+    from paper_2201_10887_b200.rbf import RbfParams
+    flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
+    for _ in render_frames([fc] * 16, g, t, RbfParams(cfg.sigma), st):
+        pass
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in render_frames([fc] * 200, g, t, RbfParams(cfg.sigma), st, before_frame=lambda i: flush.zero_()):
+        pass
+    out["pipelined_ms"] = (time.perf_counter() - t0) * 1e3 / 200
     out.update({"discretize_ms": sum(d) / len(d), "maxmip_ms": sum(m) / len(m), "render_ms": sum(r) / len(r),
                 "render_min_ms": min(r),
                 "pixels_sha": hashlib.sha256(buf.rgb.cpu().numpy().tobytes()).hexdigest()[:16],
