@@ -19,6 +19,9 @@
 //                 nodes at R=2048) and folds the partial min/max into the
 //                 job's valid range.  No atomics, no init pass: deterministic.
 // HBM traffic per job ~ 4*(R^2 + nodes) + R^2 bytes (valid), each byte once.
+// In a frame launch (hc_frame_launch) extra CTAs of the two launches also compute
+// the render's tile-queue order (hc_order.cuh: histograms in k_mip_tiles, ranked
+// scatter in k_mip_top), which needs exactly that launch boundary between them.
 #include <string.h>
 
 #include "hc_internal.cuh"
