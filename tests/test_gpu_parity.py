@@ -335,6 +335,27 @@ def test_random_pose_frame_parity(cuda, oracle, i):
     print(f"pose {i}: K={st.count} R={st.resolution} rays_hit={fr.rays_hit}")
 
 
+@pytest.mark.parametrize("R,K,overlap", [(300, 2, 5.0), (1000, 3, "auto"), (129, 5, 0.0), (777, 8, 12.5)])
+def test_odd_resolution_frame_parity(cuda, oracle, R, K, overlap):
+    """Non-power-of-two cascade resolutions (odd pyramid widths, -inf padding, partial
+    CTA tiles in every kernel), explicit overlaps and up to 8 cascades: bit-exact ray
+    casting on the GPU's rasters, exact masks/valid bits, heights within tolerance."""
+    from paper_2201_10887_b200 import render_frame
+    from paper_2201_10887_b200.rbf import RbfParams
+    from paper_2201_10887_b200.render import CascadeSettings, FrameConfig
+    cfg, g, t, fc = _config_inputs("C2", 480, 300)
+    st = CascadeSettings(resolution=R, count=K, overlap=overlap)
+    fr = render_frame(fc, g, t, RbfParams(sigma=cfg.sigma), st, debug=True)
+    assert fr.visible
+    _frame_vs_oracle(fr, oracle, fc, g)
+    for L, r in zip([L for L in fr.debug["layouts"] if L is not None], fr.debug["rasters"]):
+        o = oracle.discretize(L, g, t, cfg.sigma)
+        valid = _np(r.valid)
+        assert np.array_equal(valid, o.valid) and np.array_equal(_np(L.mask), o.mask)
+        for layer in ("terrain", "water"):
+            _check_heights(_np(r.layer(layer)), o.layer(layer), valid, f"R={R} {layer}")
+
+
 def test_division_selftest(cuda):
     """The traversal's hoisted float64 division equals IEEE a / b on 2^28 operand pairs."""
     import torch
