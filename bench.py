@@ -40,6 +40,8 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
+from paper_2201_10887_b200.configs import PATH_FRAMES  # noqa: E402
+
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 B200_SMS = 148
@@ -197,25 +199,10 @@ def build_inputs(cfg):
     return g, table, {"synth_s": round(t1 - t0, 2), "influence_table_s": round(t2 - t1, 2)}
 
 
-def rank_frame_config(cfg, rank, world):
-    """Rank r renders view r: the config camera rotated about the domain centre."""
-    if world == 1 or cfg.views > 1:
-        return cfg.frame_config(rank % max(cfg.views, 1))
-    from paper_2201_10887_b200.cascade import CameraView
-    from paper_2201_10887_b200.render import FrameConfig
-    c = cfg.camera(0)
-    ang = 2.0 * math.pi * rank / world
-    cx, cy = 1024.0, 1024.0
-    ca, sa = math.cos(ang), math.sin(ang)
-    rot = lambda p: (cx + ca * (p[0] - cx) - sa * (p[1] - cy), cy + sa * (p[0] - cx) + ca * (p[1] - cy), p[2])
-    eye, la = rot(cfg.eye), rot(cfg.look_at)
-    cam = CameraView(eye=eye, look_dir=tuple(b - a for a, b in zip(eye, la)), up=c.up, fov_y=c.fov_y,
-                     aspect=c.aspect, near_clip=c.near_clip, far_clip=c.far_clip)
-    return FrameConfig(width=cfg.width, height=cfg.height, camera=cam)
-
-
-def cpu_frames(cfg, g, table, fc, budget_s, max_frames=None):
-    """Oracle (reference CPU port) frames: returns (frames/s, per-frame stats, n).
+def cpu_frames(cfg, g, table, budget_s, max_frames=None):
+    """Oracle (reference CPU port) frames along the benchmark camera path (frame i
+    renders path pose i, as the GPU arm's step i does): returns (frames/s, last
+    frame's stats, n, median s/frame).
 
     Every frame is planned by the numpy restatement of the reference planner
     (oracle/plan_numpy.py) inside the timed frame, then discretized, ray cast and
@@ -227,11 +214,12 @@ def cpu_frames(cfg, g, table, fc, budget_s, max_frames=None):
     O.build()
     P = RbfParams(sigma=cfg.sigma)
     st = cfg.settings()
-    c = fc.camera
-    cam = PN.CameraView(eye=c.eye, look_dir=c.look_dir, up=c.up, fov_y=c.fov_y, aspect=c.aspect,
-                        near_clip=c.near_clip, far_clip=c.far_clip)
 
-    def frame():
+    def frame(i):
+        fc = cfg.path_frame_config(i)
+        c = fc.camera
+        cam = PN.CameraView(eye=c.eye, look_dir=c.look_dir, up=c.up, fov_y=c.fov_y, aspect=c.aspect,
+                            near_clip=c.near_clip, far_clip=c.far_clip)
         tp = time.perf_counter()
         plan = PN.plan_cascades(cam, g, st.resolution, st.overlap, st.count)
         plan_ms = (time.perf_counter() - tp) * 1e3
@@ -239,12 +227,12 @@ def cpu_frames(cfg, g, table, fc, budget_s, max_frames=None):
         stats["plan_ms"] = plan_ms
         return stats
 
-    frame()                                             # warm (page-in, thread pool)
+    frame(0)                                            # warm (page-in, thread pool)
     times, stats = [], None
     t_start = time.perf_counter()
     while True:
         t0 = time.perf_counter()
-        stats = frame()
+        stats = frame(len(times))
         times.append(time.perf_counter() - t0)
         if time.perf_counter() - t_start >= budget_s or (max_frames and len(times) >= max_frames):
             break
@@ -260,26 +248,49 @@ def run_reference(args, cfg):
     # scipy builder (the reference's algorithm), nothing on the GPU
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import heightcast_oracle as O
-    g = cfg.grid()
+    g = cfg.grid(native_paint=False)        # numpy tile painter: libheightcast_cuda stays unmapped
     table = O.build_influence_table(g, cfg.sigma)
-    fc = rank_frame_config(cfg, 0, 1)
-    # K frames, bounded to ~2 minutes of CPU time (C3/C4 frames take seconds each)
-    fps, stats, n, per = cpu_frames(cfg, g, table, fc, budget_s=120.0, max_frames=args.steps)
+    # K frames along the camera path, bounded to ~2 minutes of CPU time (C3/C4 frames
+    # take seconds each)
+    fps, stats, n, per = cpu_frames(cfg, g, table, budget_s=120.0, max_frames=args.steps)
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     line = {
         "impl": "reference", "metric": "frames/sec", "value": fps, "unit": "frames/s", "n_gpus": args.gpus,
         "steps": args.steps, "frames_timed": n, "warmup": args.warmup, "ms_per_step": per * 1e3,
         "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {cfg.description}", "grid_cells": g.n_cells, "cascades": cfg.cascades,
-                   "cascade_res": cfg.resolution, "image": [cfg.width, cfg.height], "sigma": cfg.sigma},
+        "config": bench_config(cfg, g, table, args.gpus),
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "port",
-                         "sample": f"{n} full {cfg.name} frames (float64 C oracle of the reference pipeline, "
-                                   f"OpenMP {cores} threads), median"},
+                         "sample": f"{n} full {cfg.name} frames along the camera path (float64 C oracle of the "
+                                   f"reference pipeline, OpenMP {cores} threads), median"},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "phases_ms": {k: round(stats[k], 3) for k in ("plan_ms", "approximation_ms", "raycast_ms")},
+        "native_so_loaded": mapped_repo_libraries(),
     }
     print(json.dumps(line), flush=True)
+
+
+def bench_config(cfg, g, table, n_gpus):
+    """`config` of both arms' JSON lines: the same dict for the same workload."""
+    d = cfg.workload(g, table)
+    d["parallelism"] = f"{'screen strips' if cfg.name == 'C5' else 'view-sharded'} x{n_gpus}"
+    d["l2"] = "GPU arm: 256 MiB L2 flush (int32 fill) between timed steps; CPU arm: none"
+    return d
+
+
+def mapped_repo_libraries():
+    """Shared objects under this repository mapped into the process (/proc/self/maps):
+    the reference arm must show only the oracle's library."""
+    out = set()
+    try:
+        with open("/proc/self/maps") as fh:
+            for line in fh:
+                path = line.split()[-1] if len(line.split()) >= 6 else ""
+                if path.endswith(".so") and path.startswith(ROOT + os.sep):
+                    out.add(os.path.relpath(path, ROOT))
+    except OSError:
+        return None
+    return sorted(out)
 
 
 def main():
@@ -290,9 +301,19 @@ def main():
         run_reference(args, cfg)
         return
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun (rank 0 prints)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={29500 + os.getpid() % 1000}", os.path.abspath(__file__)]
+        cmd += sys.argv[1:]
+        sys.stdout.flush()
+        os.execv(sys.executable, cmd)
+
     import torch
     import torch.distributed as dist
     ws, rank, local = dist_env()
+    if ws != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
@@ -308,11 +329,10 @@ def main():
     st = cfg.settings()
     P = RbfParams(sigma=cfg.sigma)
     strips = cfg.name == "C5"           # screen strips (strong scaling), else view sharding
-    if cfg.views > 1:
-        views = [cfg.frame_config(v) for v in multi.shard_views(cfg.views, ws, rank)]
-    else:
-        views = [rank_frame_config(cfg, 0 if strips else rank, ws)]
-    fc = views[0]
+    # step i renders frame i of the moving camera path (configs.path_camera): strips --
+    # every rank the same frame; views -- rank r its own (C4: views r, r+N, ...)
+    frame_of = (lambda i: cfg.path_frame_config(i)) if strips else \
+        (lambda i: cfg.path_frame_config(i, rank, ws))
     rects = multi.screen_strips(cfg.width, ws) if strips else None
     rect = (rects[rank][0], 0, rects[rank][1], cfg.height) if strips else None
     t_up = time.perf_counter()
@@ -331,12 +351,15 @@ def main():
         torch.cuda.synchronize()
 
     def step(i, events=None):
-        return enqueue_frame(views[i % len(views)], g, table, st, rect=rect, events=events)
+        return enqueue_frame(frame_of(i), g, table, st, rect=rect, events=events)
 
-    # ---- warm-up (device-resident path)
-    for i in range(max(args.warmup, 3)):
-        step(i)
+    # ---- warm-up (device-resident path): the last warm-up poses of the path, so the
+    # first timed frame's tile order comes from a different pose, as every later one does
+    n_warm = max(args.warmup, 3)
+    for i in range(-n_warm, 0):
+        step(i % (2 * PATH_FRAMES))
     torch.cuda.synchronize()
+    cnt_all = torch.zeros((args.steps, _cuda.N_COUNTERS), dtype=torch.int64, device=dev)
 
     # ---- timed: K steps, each bracketed by CUDA events (plus per-kernel events), L2
     # flushed between steps on the stream.  The host does not wait between steps, so
@@ -357,6 +380,7 @@ def main():
             ev[i][0].record()
             buf, plan, plan_ms = step(i, kh[i])
             ev[i][1].record()
+            cnt_all[i].copy_(buf.counters)       # outside the step's events (work totals)
             plan_ms_all.append(plan_ms)
         barrier()
     k_disc = [k[0].elapsed_time(k[1]) for k in kev]
@@ -373,7 +397,8 @@ def main():
     frames_per_step = 1 if strips else ws
     value = frames_per_step * args.steps / (total_ms / 1e3)
 
-    cnt = buf.counters.cpu().tolist()
+    # work per frame, averaged over the timed frames (the path changes it frame to frame)
+    cnt = (cnt_all.double().mean(dim=0)).cpu().tolist()
     work = {"pairs": cnt[_cuda.CNT_PAIRS], "node_visits": cnt[_cuda.CNT_NODE_VISITS],
             "patch_tests": cnt[_cuda.CNT_PATCH_TESTS], "valid_texels": cnt[_cuda.CNT_VALID],
             "visible_texels": cnt[_cuda.CNT_VISIBLE], "rays_hit": cnt[_cuda.CNT_RAYS_HIT]}
@@ -385,8 +410,9 @@ def main():
     # every frame.  Strips on N > 1 GPUs: render_strip + image gather per step.
     if not strips or ws == 1:
         from paper_2201_10887_b200 import render_frames
-        seq = [views[i % len(views)] for i in range(args.steps)]
-        for _ in render_frames(seq[:4] * 4, g, table, P, st):      # every buffer set, pinned blocks
+        seq = [frame_of(i) for i in range(args.steps)]
+        warm = [frame_of(i % (2 * PATH_FRAMES)) for i in range(-16, 0)]
+        for _ in render_frames(warm, g, table, P, st):      # every buffer set, pinned blocks
             pass
         barrier()
         t0 = time.perf_counter()
@@ -395,13 +421,13 @@ def main():
         e2e_ms = [(time.perf_counter() - t0) * 1e3]
     else:
         def e2e_step(i):
-            part = multi.render_strip(fc, g, table, P, st, rects[rank])
+            part = multi.render_strip(frame_of(i), g, table, P, st, rects[rank])
             img = multi.gather_strips(part, rects, rank, ws) if ws > 1 else part
             if rank == 0:
                 img.cpu()
 
-        for i in range(2):
-            e2e_step(i)
+        for i in range(-2, 0):
+            e2e_step(i % (2 * PATH_FRAMES))
         barrier()
         e2e_ms = []
         for i in range(args.steps):
@@ -475,7 +501,7 @@ def main():
     if rank == 0:
         cpu = None
         if ws == 1 and not args.no_cpu_baseline:
-            fps, stats, n, per = cpu_frames(cfg, g, table, fc, budget_s=args.cpu_seconds)
+            fps, stats, n, per = cpu_frames(cfg, g, table, budget_s=args.cpu_seconds)
             cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
             cpu = {"value": fps, "unit": "frames/s", "cores": cores, "kind": "port",
                    "sample": f"{n} full {cfg.name} frames (float64 C oracle of the reference pipeline, "
@@ -487,12 +513,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if strips else "weak",
             "vs_baseline": None, "dtype": "f64 traversal/shading, f32 RBF discretization", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: {cfg.description}", "grid_cells": g.n_cells,
-                       "mean_influence_list": round(len(table.indices) / g.n_cells, 2), "sigma": cfg.sigma,
-                       "cascades": K, "cascade_res": R, "image": [cfg.width, cfg.height],
-                       "l2": "256 MiB flush between timed steps",
-                       "parallelism": f"screen strips x{ws}" if strips else f"view-sharded x{ws}",
-                       "views_per_rank": len(views)},
+            "config": bench_config(cfg, g, table, ws),
             "rays_per_sec": value * P_pix, "layer_rays_per_sec": value * 2 * P_pix,
             "texels_per_sec": value * work["valid_texels"] / frames_per_step,
             "e2e": {"value": e2e_value, "unit": "frames/s",

@@ -330,9 +330,10 @@ typedef struct {
 size_t hc_influence_workspace_bytes(int n_cells);
 /* Two calls.  indices == NULL: counts + exclusive scan into offsets[n_cells+1]
  * (device int64), *total_out (host) = number of entries.  Then with indices
- * (device int64[total]): fill + per-list sort; *total_out (host, int32 view)
- * receives 0, or the length of a list longer than the sort capacity (error).
- * Both calls are stream-ordered; the host value is valid after a stream sync. */
+ * (device int64[capacity]): fill + per-list sort; total_out (host, read as two
+ * int32 words) receives {0 or the length of a list longer than the sort capacity,
+ * 1 if offsets[n_cells] > capacity else 0} -- nothing is written past `capacity`.
+ * Both calls are stream-ordered; the host values are valid after a stream sync. */
 int hc_influence_build(const HcGrid *grid, const HcInfluenceBins *bins, double sigma, int64_t *offsets,
                        int64_t *indices, int64_t capacity, void *workspace, size_t workspace_bytes,
                        int64_t *total_out, hc_stream_t stream);

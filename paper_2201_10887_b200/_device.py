@@ -125,7 +125,9 @@ def build_influence_gpu(grid, sigma, device=None):
         _cuda.check(L.hc_influence_build(C.byref(view), C.byref(B), sigma, offsets.data_ptr(), indices.data_ptr(),
                                          nnz, ws.data_ptr(), ws.numel(), flag.data_ptr(), s), "hc_influence_build")
         torch.cuda.current_stream().synchronize()
-    over = int(flag.numpy().view(np.int32)[0])
+    over, short = (int(x) for x in flag.numpy().view(np.int32)[:2])
+    if short:
+        raise _cuda.HeightcastCudaError(f"influence index buffer of {nnz} entries is too small")
     if over:
         raise _cuda.HeightcastCudaError(f"influence list of {over} entries exceeds the GPU sort capacity")
     table = InfluenceTable(offsets.cpu().numpy(), indices[:nnz].cpu().numpy(), sigma)

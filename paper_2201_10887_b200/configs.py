@@ -49,9 +49,62 @@ class BenchConfig:
     def frame_config(self, view: int = 0) -> FrameConfig:
         return FrameConfig(width=self.width, height=self.height, camera=self.camera(view))
 
-    def grid(self):
+    # ---- benchmark camera path (both bench.py arms render the same frames)
+
+    def path_camera(self, i: int, rank: int = 0, world: int = 1) -> CameraView:
+        """Camera of frame i of the benchmark's moving-camera path.
+
+        The reference's benchmark moves the camera every frame by lerping eye and
+        look_at between two poses (cli.py:127-131).  Here pose 1 is pose 0's eye
+        turned PATH_TURN_DEG about the look-at point; the lerp parameter runs
+        0 -> 1 -> 0 over 2 * PATH_FRAMES frames (a triangle wave, so any number of
+        steps stays on the path).  C4 cycles through its orbit views instead.
+        With world > 1 (view sharding) rank r's path is turned by 360 r / world
+        degrees about the domain centre (1024, 1024)."""
+        if self.views > 1:
+            return self.camera((i * max(world, 1) + rank) % self.views)
+        ph = i % (2 * PATH_FRAMES)
+        a = (ph if ph <= PATH_FRAMES else 2 * PATH_FRAMES - ph) / PATH_FRAMES
+        eye0, la = self.eye, self.look_at
+        ang = math.radians(PATH_TURN_DEG)
+        ca, sa = math.cos(ang), math.sin(ang)
+        ex, ey = eye0[0] - la[0], eye0[1] - la[1]
+        eye1 = (la[0] + ca * ex - sa * ey, la[1] + sa * ex + ca * ey, eye0[2])
+        eye = tuple((1 - a) * p + a * q for p, q in zip(eye0, eye1))
+        if world > 1:
+            rot = 2.0 * math.pi * rank / world
+            cr, sr = math.cos(rot), math.sin(rot)
+            turn = lambda p: (1024.0 + cr * (p[0] - 1024.0) - sr * (p[1] - 1024.0),
+                              1024.0 + sr * (p[0] - 1024.0) + cr * (p[1] - 1024.0), p[2])
+            eye, la = turn(eye), turn(la)
+        look = tuple(b - p for p, b in zip(eye, la))
+        return CameraView(eye=eye, look_dir=look, up=(0.0, 0.0, 1.0), fov_y=55.0,
+                          aspect=self.width / self.height, near_clip=1.0, far_clip=6000.0)
+
+    def path_frame_config(self, i: int, rank: int = 0, world: int = 1) -> FrameConfig:
+        return FrameConfig(width=self.width, height=self.height, camera=self.path_camera(i, rank, world))
+
+    def workload(self, grid=None, table=None) -> dict:
+        """The `config` dict of a bench.py line (identical in both arms)."""
+        d = {"workload": f"{self.name}: {self.description}", "sigma": self.sigma, "cascades": self.cascades,
+             "cascade_res": self.resolution, "image": [self.width, self.height],
+             "camera_path": (f"{self.views} orbit views, cycled" if self.views > 1 else
+                             f"eye lerped {PATH_TURN_DEG:g} deg about look_at and back over "
+                             f"{2 * PATH_FRAMES} frames (cli.py:127-131 style), one pose per step")}
+        if grid is not None:
+            d["grid_cells"] = grid.n_cells
+        if table is not None and grid is not None:
+            d["mean_influence_list"] = round(len(table.indices) / max(grid.n_cells, 1), 2)
+        return d
+
+    def grid(self, native_paint: bool = True):
         from .synth import generate_synthetic
-        return generate_synthetic(self.kind, self.seed, self.cells, max_depth=self.max_depth)
+        return generate_synthetic(self.kind, self.seed, self.cells, max_depth=self.max_depth,
+                                  native_paint=native_paint)
+
+
+PATH_FRAMES = 60          # frames from pose 0 to pose 1 of the benchmark camera path
+PATH_TURN_DEG = 45.0      # pose 1: pose 0's eye turned about the look-at point
 
 
 CONFIGS = {

@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(32 * INF_WARPS) k_influence_count(const __grid
 __global__ void __launch_bounds__(32 * INF_WARPS) k_influence_fill(const __grid_constant__ InfluenceParams P,
                                                                   const int64_t* __restrict__ offsets,
                                                                   int64_t* __restrict__ indices,
+                                                                  int64_t capacity,
                                                                   int32_t* __restrict__ overflow) {
     __shared__ int32_t lists[INF_WARPS][INF_LIST_CAP];
     const int w = threadIdx.x >> 5;
@@ -91,6 +92,10 @@ __global__ void __launch_bounds__(32 * INF_WARPS) k_influence_fill(const __grid_
     if (a >= P.n_cells) return;
     const int64_t beg = offsets[a];
     const int n = (int)(offsets[a + 1] - beg);
+    if (offsets[a + 1] > capacity) {       // caller's indices buffer too small: write nothing
+        if (lane == 0) atomicMax(overflow + 1, 1);
+        return;
+    }
     if (n > INF_LIST_CAP) {
         if (lane == 0) atomicMax(overflow, n);
         return;
@@ -160,7 +165,7 @@ extern "C" int hc_influence_build(const HcGrid* grid, const HcInfluenceBins* bin
     P.sigma = sigma;
     const int blocks = (n + INF_WARPS - 1) / INF_WARPS;
     if (indices == nullptr) {   // pass 1: counts -> offsets, total
-        // counts land in offsets[1..n]; scanned in place into offsets[0..n]
+        // counts land in offsets[0..n-1], offsets[n] is zeroed; scanned in place into offsets[0..n]
         k_influence_count<<<blocks, 32 * INF_WARPS, 0, s>>>(P, offsets);
         int rc = cuda_status("hc_influence_build(count)");
         if (rc) return rc;
@@ -173,13 +178,14 @@ extern "C" int hc_influence_build(const HcGrid* grid, const HcInfluenceBins* bin
         cudaMemcpyAsync(total_out, offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
         return cuda_status("hc_influence_build(scan)");
     }
-    // pass 2: fill (offsets from pass 1); total_out receives the overflow length (0 = ok)
-    HC_REQUIRE(workspace && workspace_bytes >= sizeof(int32_t), "hc_influence_build: workspace too small");
+    // pass 2: fill (offsets from pass 1).  total_out (host, two int32 words) receives
+    // {length of a list past the sort capacity or 0, 1 if offsets[n] > capacity else 0};
+    // lists that would end past `capacity` are not written.
+    HC_REQUIRE(capacity >= 0, "hc_influence_build: negative capacity");
+    HC_REQUIRE(workspace && workspace_bytes >= 2 * sizeof(int32_t), "hc_influence_build: workspace too small");
     int32_t* overflow = (int32_t*)workspace;
-    cudaMemsetAsync(overflow, 0, sizeof(int32_t), s);
-    k_influence_fill<<<blocks, 32 * INF_WARPS, 0, s>>>(P, offsets, indices, overflow);
-    int32_t* host_over = (int32_t*)total_out;
-    cudaMemcpyAsync(host_over, overflow, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-    (void)capacity;
+    cudaMemsetAsync(overflow, 0, 2 * sizeof(int32_t), s);
+    k_influence_fill<<<blocks, 32 * INF_WARPS, 0, s>>>(P, offsets, indices, capacity, overflow);
+    cudaMemcpyAsync(total_out, overflow, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
     return cuda_status("hc_influence_build(fill)");
 }

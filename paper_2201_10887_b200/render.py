@@ -227,7 +227,13 @@ def render_frames(configs, grid: AdaptiveGrid, table: InfluenceTable, params: Rb
     discretization and mips run while earlier frames' ray casting finishes (whose
     last long rays leave most SMs idle), and pixels are read back on a copy stream
     meanwhile.  `before_frame(i)`, if given, is called on frame i's stream before
-    it is enqueued (e.g. to enqueue an L2 flush)."""
+    it is enqueued (e.g. to enqueue an L2 flush); with depth > 1 it runs while
+    earlier frames are still in flight, not between frames.
+
+    Per-frame `approximation_ms` / `raycast_ms` are event intervals on the frame's
+    own stream: with depth > 1 other frames share the SMs during them, so they
+    overlap and are not the times of a frame rendered alone (use depth=1 for
+    per-phase timing, as `render_frame` does)."""
     import collections
     import torch
     if table.sigma != params.sigma:
@@ -248,36 +254,42 @@ def render_frames(configs, grid: AdaptiveGrid, table: InfluenceTable, params: Rb
             st.wait_stream(caller)         # side streams start after the caller's prior work
         read_done = [None] * depth         # per buffer slot: its last read-back
         pending = collections.deque()
-        for i, config in enumerate(configs):
-            slot = i % depth
-            compute = streams[slot]
-            with torch.cuda.stream(compute):
-                if before_frame is not None:
-                    before_frame(i)
-                if read_done[slot] is not None:
-                    compute.wait_event(read_done[slot])  # slot's previous pixels copied out
-                queued = enqueue_frame(config, grid, table, settings, slot=slot)
-            if queued is None:
-                pending.append(("background", config))
-            else:
-                buf, plan, plan_ms = queued
-                done = torch.cuda.Event()
-                done.record(compute)
-                pixels = torch.empty((config.height, config.width, 3), dtype=torch.uint8, pin_memory=True)
-                counters = torch.empty(_cuda.N_COUNTERS, dtype=torch.int64, pin_memory=True)
-                with torch.cuda.stream(copy):
-                    copy.wait_event(done)
-                    pixels.copy_(buf.rgb, non_blocking=True)
-                    counters.copy_(buf.counters, non_blocking=True)
-                    read_done[slot] = torch.cuda.Event()
-                    read_done[slot].record(copy)
-                pending.append(("frame", buf, plan, plan_ms, pixels, counters, read_done[slot]))
-            if len(pending) >= depth:
+        try:
+            for i, config in enumerate(configs):
+                slot = i % depth
+                compute = streams[slot]
+                with torch.cuda.stream(compute):
+                    if before_frame is not None:
+                        before_frame(i)
+                    if read_done[slot] is not None:
+                        compute.wait_event(read_done[slot])  # slot's previous pixels copied out
+                    queued = enqueue_frame(config, grid, table, settings, slot=slot)
+                if queued is None:
+                    pending.append(("background", config))
+                else:
+                    buf, plan, plan_ms = queued
+                    done = torch.cuda.Event()
+                    done.record(compute)
+                    pixels = torch.empty((config.height, config.width, 3), dtype=torch.uint8, pin_memory=True)
+                    counters = torch.empty(_cuda.N_COUNTERS, dtype=torch.int64, pin_memory=True)
+                    with torch.cuda.stream(copy):
+                        copy.wait_event(done)
+                        pixels.copy_(buf.rgb, non_blocking=True)
+                        counters.copy_(buf.counters, non_blocking=True)
+                        read_done[slot] = torch.cuda.Event()
+                        read_done[slot].record(copy)
+                    pending.append(("frame", buf, plan, plan_ms, pixels, counters, read_done[slot]))
+                if len(pending) >= depth:
+                    yield _finish_pending(pending.popleft(), grid, params)
+            while pending:
                 yield _finish_pending(pending.popleft(), grid, params)
-        for st in streams[1:]:
-            caller.wait_stream(st)         # later work on the caller's stream sees every frame
-        while pending:
-            yield _finish_pending(pending.popleft(), grid, params)
+        finally:
+            # also when the consumer stops early (GeneratorExit at a yield): later work
+            # on the caller's stream -- including the caching allocator's reuse of memory
+            # freed there -- must see every side-stream frame and read-back
+            for st in streams[1:]:
+                caller.wait_stream(st)
+            caller.wait_stream(copy)
 
 
 def _finish_pending(item, grid, params):

@@ -23,3 +23,25 @@ def test_reference_arm_json_contract():
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert d["e2e"] == {"value": d["value"], "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert d["config"]["workload"].startswith("C1")
+    # the arm runs oracle code only: the product library is never mapped (/proc/self/maps)
+    assert d["native_so_loaded"] == ["oracle/liboracle.so"], d["native_so_loaded"]
+
+
+def test_both_arms_share_config_and_camera_path():
+    """The GPU arm's and the reference arm's `config` dicts are built by the same
+    function; the camera path moves every frame (cli.py:127-131)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2201_10887_b200.configs import CONFIGS, PATH_FRAMES
+    cfg = CONFIGS["C2"]
+    a = bench.bench_config(cfg, None, None, 1)
+    b = bench.bench_config(cfg, None, None, 1)
+    assert a == b and a["camera_path"]
+    eyes = [cfg.path_camera(i).eye for i in range(2 * PATH_FRAMES + 1)]
+    assert eyes[0] == eyes[2 * PATH_FRAMES] == cfg.eye
+    assert all(eyes[i] != eyes[i + 1] for i in range(2 * PATH_FRAMES))
+    # view sharding: ranks see different poses of the same step
+    assert cfg.path_camera(5, 0, 2).eye != cfg.path_camera(5, 1, 2).eye
+    c4 = CONFIGS["C4"]
+    assert {c4.path_camera(i, r, 4).eye for i in range(16) for r in range(4)} == \
+        {c4.camera(v).eye for v in range(64)}
