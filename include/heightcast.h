@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define HC_ABI_VERSION 3
+#define HC_ABI_VERSION 4
 #define HC_MAX_EDGES 32      /* polygon edges per cascade mask          */
 #define HC_MAX_CASCADES 8    /* K (the reference hard-codes 3)           */
 #define HC_MAX_LEVELS 20     /* max-mip levels (R <= 2^19)               */
@@ -58,8 +58,11 @@ typedef void *hc_stream_t;   /* cudaStream_t */
  * terrain_i - terrain_head, depth_i - depth_head} (float32), stored as pairs of
  * consecutive list entries so two records feed one packed f32x2 operation:
  * cell a's pairs are [pair_offsets[a], pair_offsets[a+1]), pair p of the list
- * holding entries 2p and 2p+1 (an odd list's last pair is padded with a record
- * of weight exactly 0). */
+ * holding entries 2p and 2p+1.  Every list has a multiple of 4 pairs (padded
+ * with records of weight exactly 0) and is stored as quads of pairs, 160 bytes
+ * each: float4 {x0,x1,y0,y1} x4, float4 {s0,s1,t0,t1} x4, float2 {d0,d1} x4 --
+ * so a list (or any run of whole quads) is one contiguous 16-byte-aligned range,
+ * one TMA bulk copy. */
 typedef struct {
     const double *cx, *cy, *size, *terrain, *depth;   /* [n_cells] */
     const int32_t *tile_index;                         /* [nty][ntx] */
@@ -68,10 +71,9 @@ typedef struct {
     int32_t n_cells;
     const int32_t *offsets;                            /* [n_cells+1] */
     const int32_t *indices;                            /* [offsets[n]] */
-    const int32_t *pair_offsets;                       /* [n_cells+1] prefix of ceil(list length / 2) */
-    const float *rec_xy;                               /* [pairs][4] {x0, x1, y0, y1} */
-    const float *rec_st;                               /* [pairs][4] {s0, s1, t0, t1} */
-    const float *rec_d;                                /* [pairs][2] {d0, d1} */
+    const int32_t *pair_offsets;                       /* [n_cells+1] prefix of ceil(list length / 2),
+                                                          each term rounded up to a multiple of 4 */
+    const float *rec;                                  /* [pairs / 4][40] quads of record pairs */
     const float *anchor_t, *anchor_d;                  /* [n_cells] terrain/depth of list head, f32 */
     double sigma;
 } HcGrid;
@@ -249,8 +251,7 @@ const char *hc_last_error(void);
 
 /* Anchored influence records from the CSR table (startup precompute; replaces the
  * per-batch gather of discretize.py:111-119 + rbf.py:109-123 operand setup). */
-int hc_build_records(const HcGrid *grid, float *rec_xy, float *rec_st, float *rec_d, float *anchor_t,
-                     float *anchor_d, hc_stream_t stream);
+int hc_build_records(const HcGrid *grid, float *rec, float *anchor_t, float *anchor_d, hc_stream_t stream);
 
 /* Visibility mask only (cascade.py:507-521).  mask is [R][R] uint8. */
 int hc_visibility_mask(const HcCascadeRaster *c, hc_stream_t stream);

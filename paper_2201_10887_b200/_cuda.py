@@ -17,7 +17,7 @@ LIB_DIR = os.path.join(PKG_DIR, "_lib")
 LIB_PATH = os.environ.get("HC_LIB_PATH") or os.path.join(LIB_DIR, "libheightcast_cuda.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 
-HC_ABI_VERSION = 3
+HC_ABI_VERSION = 4
 HC_MAX_EDGES = 32
 HC_MAX_CASCADES = 8
 HC_MAX_LEVELS = 20
@@ -68,8 +68,7 @@ class HcGrid(C.Structure):
     _fields_ = [("cx", _vp), ("cy", _vp), ("size", _vp), ("terrain", _vp), ("depth", _vp),
                 ("tile_index", _vp), ("ntx", _i64), ("nty", _i64),
                 ("xmin", _d), ("ymin", _d), ("min_cell", _d), ("n_cells", _i32),
-                ("offsets", _vp), ("indices", _vp), ("pair_offsets", _vp), ("rec_xy", _vp),
-                ("rec_st", _vp), ("rec_d", _vp),
+                ("offsets", _vp), ("indices", _vp), ("pair_offsets", _vp), ("rec", _vp),
                 ("anchor_t", _vp), ("anchor_d", _vp), ("sigma", _d)]
 
 
@@ -186,7 +185,7 @@ def lib():
                                    ROOT_FN, C.POINTER(HcPlan)]
     L.hc_maxmip_workspace_bytes.restype = C.c_size_t
     L.hc_maxmip_workspace_bytes.argtypes = [C.c_int, C.c_int]
-    L.hc_build_records.argtypes = [C.POINTER(HcGrid), _vp, _vp, _vp, _vp, _vp, _vp]
+    L.hc_build_records.argtypes = [C.POINTER(HcGrid), _vp, _vp, _vp, _vp]
     L.hc_visibility_mask.argtypes = [C.POINTER(HcCascadeRaster), _vp]
     L.hc_discretize.argtypes = [C.POINTER(HcCascadeRaster), C.c_int, C.POINTER(HcGrid), C.c_float,
                                 _vp, _vp]

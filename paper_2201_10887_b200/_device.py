@@ -10,9 +10,10 @@ Layout in HBM:
   tile_index                     int32 [nty, ntx]  min-cell lookup (grid.py:154-177)
   offsets                        int32 [N+1]       CSR (grid.py:350-376)
   indices                        int32 [N*L]
-  pair_offsets                   int32 [N+1]       prefix of ceil(list length / 2)
-  rec_xy, rec_st                 float32 [pairs, 4] {x0, x1, y0, y1}, {s0, s1, t0, t1}
-  rec_d                          float32 [pairs, 2] {d0, d1}  (pairs of consecutive list entries)
+  pair_offsets                   int32 [N+1]       prefix of ceil(list length / 2), each rounded up to x4
+  rec                            float32 [pairs/4, 40] quads of record pairs (pairs of consecutive
+                                                   list entries): {x0,x1,y0,y1} x4, {s0,s1,t0,t1} x4,
+                                                   {d0,d1} x4
   anchor_t, anchor_d             float32 [N]       list-head terrain / depth
 """
 
@@ -42,21 +43,20 @@ class InfluenceDevice:
             self.indices = torch.from_numpy(table.indices.astype(np.int32)).to(dev)
         n = gdev.n_cells
         lens = np.diff(np.asarray(table.offsets, dtype=np.int64))
+        # pairs of list entries, padded to a multiple of 4 pairs: every list is a run
+        # of whole 160-byte quads (one TMA bulk copy, 16-byte aligned)
         pair_off = np.zeros(n + 1, dtype=np.int64)
-        np.cumsum((lens + 1) // 2, out=pair_off[1:])
+        np.cumsum((((lens + 1) // 2) + 3) & ~3, out=pair_off[1:])
         if pair_off[-1] >= 2 ** 31:
             raise ValueError("influence table too large for int32 device indexing")
         self.pair_offsets = torch.from_numpy(pair_off.astype(np.int32)).to(dev)
         n_pairs = max(int(pair_off[-1]), 1)
-        self.rec_xy = torch.empty((n_pairs, 4), dtype=torch.float32, device=dev)
-        self.rec_st = torch.empty((n_pairs, 4), dtype=torch.float32, device=dev)
-        self.rec_d = torch.empty((n_pairs, 2), dtype=torch.float32, device=dev)
+        self.rec = torch.empty((max(n_pairs // 4, 1), 40), dtype=torch.float32, device=dev)
         self.anchor_t = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
         self.anchor_d = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
         self.view = gdev.hc_grid(self)
         with torch.cuda.device(dev):
-            _cuda.check(_cuda.lib().hc_build_records(C.byref(self.view), self.rec_xy.data_ptr(),
-                                                     self.rec_st.data_ptr(), self.rec_d.data_ptr(),
+            _cuda.check(_cuda.lib().hc_build_records(C.byref(self.view), self.rec.data_ptr(),
                                                      self.anchor_t.data_ptr(),
                                                      self.anchor_d.data_ptr(),
                                                      _cuda.stream_ptr()), "hc_build_records")
@@ -172,7 +172,7 @@ class GridDevice:
         if inf is not None:
             g.offsets, g.indices = inf.offsets.data_ptr(), inf.indices.data_ptr()
             g.pair_offsets = inf.pair_offsets.data_ptr()
-            g.rec_xy, g.rec_st, g.rec_d = inf.rec_xy.data_ptr(), inf.rec_st.data_ptr(), inf.rec_d.data_ptr()
+            g.rec = inf.rec.data_ptr()
             g.anchor_t, g.anchor_d = inf.anchor_t.data_ptr(), inf.anchor_d.data_ptr()
             g.sigma = inf.sigma
         return g

@@ -25,9 +25,10 @@ _L = np.array([-0.45, -0.35, 0.82])
 LIGHT_DIR = _L / np.linalg.norm(_L)               # render.py:35-36
 COLOR_STOPS = np.array([(0.0, 0.0, 128.0), (0.0, 180.0, 220.0), (240.0, 248.0, 255.0)])
 
-# hc_frame_launch: discretize (1) + max mips (2, which also compute the render's tile
-# order in extra CTAs) + render (1)
-LAUNCHES_PER_FRAME = 4
+# hc_frame_launch: discretize with fused mip levels 0..5 (1) + mip levels >= 6 and
+# valid ranges (1) -- both also compute the render's tile order in extra CTAs -- +
+# render (1)
+LAUNCHES_PER_FRAME = 3
 
 
 def mip_shape(R: int):

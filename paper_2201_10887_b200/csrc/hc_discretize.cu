@@ -1,95 +1,154 @@
-// hc_discretize.cu -- visibility mask, cell lookup and Eq. 1/2 discretization.
+// hc_discretize.cu -- visibility mask, cell lookup, Eq. 1/2 discretization and
+// (in a frame) the first six max-mip levels, in one launch.
 //
-// Replaces, per frame and for all K cascades in one launch:
+// Replaces, per frame and for all K cascades:
 //   cascade.py:507-521      _visibility_mask (float64, exact: no FMA, host hypot)
 //   discretize.py:63-77     texel centres origin + i*texel, cells_at, inside test
 //   grid.py:200-210         floor((x - xmin)/mc) -> tile index
 //   discretize.py:79-108    grouped Eq. 2 evaluation with sentinel / valid
 //   rbf.py:77-130           truncated-Gaussian weights + anchored sums
+//   raycast.py:61-88        max-mip levels 0..5 (fused epilogue, frame launches)
+//   discretize.py:44-49     valid height range (per-CTA partials)
 //
-// Design (B200): one thread per texel, warps own 8x4 texel tiles, blocks 16x16.
-//  * Block classification: a block whose texels provably all fail (or all pass)
-//    the mask's edge tests skips the per-texel float64 tests (classify_block);
-//    86 % of C3's cascade texels lie outside the mask polygon.
-//  * Records: each CSR entry is a precomputed anchored record (hc_build_records):
-//    the influencer's centre relative to the containing cell's centre, the
-//    Gaussian exponent scale, and value differences to the list head (the
-//    reference's anchor, rbf.py:119-123), stored as pairs of consecutive entries
-//    so two records feed one packed f32x2 FADD2/FMUL2/FFMA2 (same per-element
-//    rounding as scalar code).  The texel's offset to its cell centre is computed
-//    in float64 and rounded once, so float32 distances keep ~1 ulp relative
-//    accuracy on 2 km domains.  exp is one MUFU ex2 per record.
-//  * Warps whose texels fall in at most STAGE_GROUPS cells (C3: 91 % of warps)
-//    stream those cells' lists cooperatively -- coalesced cp.async copies of 64
-//    record pairs per chunk into a per-warp double buffer in shared memory, the
-//    next chunk in flight while the current one is consumed -- and every lane
-//    reads its own cell's records from shared memory.  With per-lane loads all
-//    lanes of such a warp fetch the same address, keeping only a few hundred
-//    bytes in flight per warp (C3 ran DRAM-latency-bound at ~1.3 TB/s).
-//  * Other warps gather per lane (32 distinct lists in flight), after an
-//    asynchronous bulk L2 prefetch of each lane's whole list.
-// Per-texel summation order is the list order, so rasters are deterministic and
-// independent of the launch shape.
+// Design (B200).  One CTA per 32x32 texel block of a cascade, 8 warps.
+//  1. Classification: warp 0 tests the block's corner box against the mask
+//     polygon (classify_block); a block provably outside writes sentinels (and
+//     sentinel mips) and leaves; a block provably inside skips the per-texel
+//     float64 edge tests.
+//  2. Cell lookup (the per-tile cell list): every texel of the
+//     block's region -- 33x33 in a frame launch, the block plus a one-texel halo
+//     so the level-0 mip nodes on the block's right/top edge see both corners --
+//     gets its containing cell, its record range and its float32 offset to the
+//     cell centre, in shared memory.  All of the block's dependent global loads
+//     (tile index -> cell SoA / CSR offsets) happen here, for all texels at once.
+//  3. Evaluation: the region is split into units of 32 texels (8x4 tiles, plus
+//     the halo row, column and corner).  Warps take units from a CTA counter.
+//     A unit whose texels lie in at most 8 cells streams those cells' record
+//     lists through a per-warp double buffer in shared memory with TMA bulk
+//     copies (cp.async.bulk, one mbarrier per buffer); the first chunk of the
+//     warp's next unit is issued while the current unit's last chunk is
+//     consumed, so the pipeline never drains between units.  Each lane reads its
+//     own cell's records from shared memory.  Other units gather per lane from
+//     global memory after an L2 bulk prefetch of each lane's list.
+//     Records come as pairs of list entries so two records share one packed
+//     f32x2 FADD2/FMUL2/FFMA2; Eq. 1 is one MUFU ex2 per record; the two records
+//     of a pair accumulate into separate partial sums (packed), added at the end.
+//  4. Epilogue: owned texels are written with coalesced stores; in a frame
+//     launch the block also reduces mip levels 0..5 of both layers in shared
+//     memory, writes the patch bytes (all four corners valid; a corner differs
+//     between the layers) and its partial valid-height min/max.  k_mip_top
+//     (hc_maxmip.cu) finishes levels >= 6 and folds the partials.
+// The sum order per texel is fixed (the list order, alternating between the two
+// partial sums), so rasters are deterministic and independent of the launch
+// shape, of the unit a texel is evaluated in and of the path (staged or
+// gathered): a halo texel computed by a neighbour equals the owner's value.
 #include <math.h>
+#include <string.h>
 
 #include "hc_internal.cuh"
+#include "hc_order.cuh"
 
 namespace hc {
 
 // -0.5 * log2(e): exp(-r2/2) = ex2(r2u * k_i) with k_i = NEG_HALF_LOG2E / (sigma c_i)^2
 constexpr double NEG_HALF_LOG2E = -0.72134752044448170368;
-// r2 >= 12.25 <=> q = r2 * NEG_HALF_LOG2E <= 12.25 * NEG_HALF_LOG2E
+// r2 >= 12.25 (3.5 sigma, rbf.py:29-32) <=> q = r2 * NEG_HALF_LOG2E <= Q_CUT
 constexpr float Q_CUT = (float)(12.25 * NEG_HALF_LOG2E);
-// exp(-3.5^2 / 2) (rbf.py:30)
-constexpr float REMAINDER_F = 2.187491118182885e-03f;
 #ifndef DISC_BATCH
 #define DISC_BATCH 4               // record pairs per batch of the per-lane path
 #endif
-constexpr int STAGE_PAIRS = 64;    // record pairs per warp buffer, shared by up to STAGE_GROUPS cells
-#ifndef DISC_STAGE_GROUPS
-#define DISC_STAGE_GROUPS 8
+#ifndef DISC_STAGE_PAIRS
+#define DISC_STAGE_PAIRS 128       // 2 CTAs per SM (76: 3 CTAs per SM, measured slower)
 #endif
-constexpr int STAGE_GROUPS = DISC_STAGE_GROUPS;
+#ifndef DISC_MIN_CTAS
+#define DISC_MIN_CTAS 2
+#endif
+constexpr int STAGE_PAIRS = DISC_STAGE_PAIRS;   // record pairs per warp buffer, shared by up to STAGE_GROUPS cells
+constexpr int STAGE_GROUPS = 8;
 constexpr int DISC_WARPS = 8;
+constexpr int BLK = 32;            // texels per block side (= level-5 mip node)
+constexpr int TILE_LEVELS = 6;     // mip levels 0..5 reduced per block
+constexpr int QUAD = 10;           // float4 per quad of record pairs (heightcast.h HcGrid.rec)
+// pairs per group slot and chunk for ng groups: floor(STAGE_PAIRS / ng) rounded down to whole quads
+__host__ __device__ constexpr int group_chunk(int ng) { return (STAGE_PAIRS / ng) & ~3; }
+// float4 per buffer: max over ng of ng * (chg / 4 * QUAD + 1) (one odd pad per group slot
+// spreads the groups' slots over the shared-memory banks)
+constexpr int stage_f4() {
+    int m = 0;
+    for (int ng = 1; ng <= STAGE_GROUPS; ++ng) {
+        const int v = ng * (group_chunk(ng) / 4 * QUAD + 1);
+        m = v > m ? v : m;
+    }
+    return m;
+}
+constexpr int STAGE_F4 = stage_f4();
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
-                 "l"(gmem)
+// ---------------------------------------------------------------------------
+// TMA bulk copy + mbarrier (sm_90+ PTX; SASS UBLKCP / SYNCS)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
-                 "l"(gmem)
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared bulk copy (bytes multiple of 16, both addresses 16-byte aligned),
+// completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(smem)),
+                 "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-// asynchronous DRAM -> L2 prefetch of a byte range (TMA unit; no registers, no completion)
+// order this thread's earlier generic-proxy accesses of shared memory before later
+// async-proxy (TMA) writes to it
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// asynchronous DRAM -> L2 prefetch of a byte range (no registers, no completion)
 __device__ __forceinline__ void prefetch_l2(const void* p, int bytes) {
     const uintptr_t a0 = (uintptr_t)p & ~(uintptr_t)15;
     const uintptr_t a1 = ((uintptr_t)p + (uintptr_t)bytes + 15) & ~(uintptr_t)15;
     if (a1 > a0)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
 }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 
-struct DiscretizeParams {
+struct DiscParams {
     HcCascadeRaster c[HC_MAX_CASCADES];
     int32_t n_cascades;
     float sentinel;
     unsigned long long* counters;
+    int32_t blocks_side;            // blocks per cascade side (ceil(R_max / 32))
+    int32_t n_blocks;               // n_cascades * blocks_side^2; CTAs past it build the tile-queue histogram
+    // fused max-mip epilogue (frame launches): level L of cascade k, layer l at mip[k][l] + level_off[L]
+    float* mip[HC_MAX_CASCADES][2];
+    uint8_t* patch_ok[HC_MAX_CASCADES];
+    int32_t n_levels;
+    int32_t max_tiles;              // partial slots per job (blocks_side^2)
+    int64_t level_off[TILE_LEVELS];
+    int32_t level_w[TILE_LEVELS];
+    float* partial;                 // [2K][max_tiles][2] valid min/max per block
+    int32_t full_mips;              // 0: blocks outside the mask write only their top node (see below)
+    OrderJob ord;                   // tile-queue order histogram of the frame's k_render (n_tiles 0: none)
 };
 
-// ---------------------------------------------------------------------------
-
-// Pair-interleaved anchored records (see heightcast.h HcGrid): one warp per cell,
-// one lane per record pair; an odd list's last pair gets a neutral second record
-// (x = 1e15, scale = -1e30: q = -inf, weight exactly 0, t = d = 0) so the pair loop
-// needs no tail and the sums are unchanged bit for bit.
-__global__ void __launch_bounds__(256) k_build_records(HcGrid g, float4* __restrict__ rec_xy,
-                                                       float4* __restrict__ rec_st, float2* __restrict__ rec_d,
+// Pair-interleaved anchored records in quads (see heightcast.h HcGrid): one warp per
+// cell, one lane per record pair; pairs past the list (an odd list's last pair, and
+// the pad pairs that make every list a whole number of quads) get neutral records
+// (x = 1e15, scale = -1e30: q = -inf, weight exactly 0, t = d = 0), so the kernel
+// evaluates whole quads and the sums are unchanged bit for bit.
+__global__ void __launch_bounds__(256) k_build_records(HcGrid g, float4* __restrict__ rec,
                                                        float* __restrict__ anchor_t,
                                                        float* __restrict__ anchor_d) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -122,9 +181,10 @@ __global__ void __launch_bounds__(256) k_build_records(HcGrid g, float4* __restr
                 x[k] = 1e15f, y[k] = 0.f, sc[k] = -1e30f, t[k] = 0.f, d[k] = 0.f;
             }
         }
-        rec_xy[p] = make_float4(x[0], x[1], y[0], y[1]);
-        rec_st[p] = make_float4(sc[0], sc[1], t[0], t[1]);
-        rec_d[p] = make_float2(d[0], d[1]);
+        float4* q = rec + (int64_t)(p >> 2) * QUAD;
+        q[p & 3] = make_float4(x[0], x[1], y[0], y[1]);
+        q[4 + (p & 3)] = make_float4(sc[0], sc[1], t[0], t[1]);
+        reinterpret_cast<float2*>(q + 8)[p & 3] = make_float2(d[0], d[1]);
     }
 }
 
@@ -155,7 +215,7 @@ __device__ __forceinline__ int containing_cell(const HcGrid& g, double px, doubl
     const double fx = floor(inv != 0.0 ? dmul(qx, inv) : ddiv(qx, g.min_cell));
     const double fy = floor(inv != 0.0 ? dmul(qy, inv) : ddiv(qy, g.min_cell));
     if (!(fx >= 0.0 && fy >= 0.0 && fx < (double)g.ntx && fy < (double)g.nty)) return -1;
-    return g.tile_index[(int64_t)fy * g.ntx + (int64_t)fx];
+    return __ldg(g.tile_index + (int64_t)fy * g.ntx + (int64_t)fx);
 }
 
 __global__ void __launch_bounds__(256) k_visibility_mask(HcCascadeRaster c) {
@@ -167,16 +227,16 @@ __global__ void __launch_bounds__(256) k_visibility_mask(HcCascadeRaster c) {
     c.mask[(int64_t)iy * c.resolution + ix] = texel_visible(c, px, py) ? 1 : 0;
 }
 
-// Classify a block of texels [x0, x1] x [y0, y1] against the mask polygon without
-// testing every texel (86 % of C3's cascade texels lie outside the polygon).  The
-// computed texel centres are monotone in the index, so they lie in the box spanned
-// by the corner centres; each edge test is the rounded value of a linear function
-// L(p) = e_x (p_y - a_y) - e_y (p_x - a_x), whose extremes over the box are at the
-// corners, and every rounded evaluation (texel or corner) is within
-// 2^-45 (|e_x|(|p_y|+|a_y|) + |e_y|(|p_x|+|a_x|)) of L (three roundings of at most
-// 2^-53 relative each).  An edge that fails at all four corners by more than twice
-// that bound fails for every texel; an edge that passes by that margin everywhere
-// passes for every texel.  Returns 0 = all outside, 1 = all inside, 2 = test texels.
+// Classify a box of texels [x0, x1] x [y0, y1] against the mask polygon without
+// testing every texel.  The computed texel centres are monotone in the index, so
+// they lie in the box spanned by the corner centres; each edge test is the
+// rounded value of a linear function L(p) = e_x (p_y - a_y) - e_y (p_x - a_x),
+// whose extremes over the box are at the corners, and every rounded evaluation
+// (texel or corner) is within 2^-45 (|e_x|(|p_y|+|a_y|) + |e_y|(|p_x|+|a_x|)) of L
+// (three roundings of at most 2^-53 relative each).  An edge that fails at all
+// four corners by more than twice that bound fails for every texel; an edge that
+// passes by that margin everywhere passes for every texel.  Returns 0 = all
+// outside, 1 = all inside, 2 = test texels.  Called by one whole warp.
 __device__ int classify_block(const HcCascadeRaster& c, int x0, int y0, int x1, int y1, int lane) {
     const double qx0 = dadd(c.origin_x, dmul((double)x0, c.texel)), qx1 = dadd(c.origin_x, dmul((double)x1, c.texel));
     const double qy0 = dadd(c.origin_y, dmul((double)y0, c.texel)), qy1 = dadd(c.origin_y, dmul((double)y1, c.texel));
@@ -203,213 +263,541 @@ __device__ int classify_block(const HcCascadeRaster& c, int x0, int y0, int x1, 
     return fail_all ? 0 : (pass_all ? 1 : 2);
 }
 
-__global__ void __launch_bounds__(256) k_discretize(const __grid_constant__ DiscretizeParams P,
-                                                    const __grid_constant__ HcGrid g) {
-    const HcCascadeRaster& c = P.c[blockIdx.z];
-    const int R = c.resolution;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // block = 16x16 texels as 2 x 4 warp tiles of 8 x 4
-    const int ix = blockIdx.x * 16 + (warp & 1) * 8 + (lane & 7);
-    const int iy = blockIdx.y * 16 + (warp >> 1) * 4 + (lane >> 3);
-    if (blockIdx.x * 16 >= (unsigned)R || blockIdx.y * 16 >= (unsigned)R) return;
-    const bool in_raster = ix < R && iy < R;
-    const int64_t o = (int64_t)iy * R + ix;
+// Accumulators of one texel: the two records of a pair go to the .x / .y halves.
+struct Acc {
+    float2 w, t, d;
+};
 
-    // warp 0 classifies the block (a per-warp copy of the classification was measured slower)
-    __shared__ int s_cls;
-    if (warp == 0) {
-        const int cls = classify_block(c, blockIdx.x * 16, blockIdx.y * 16, min((int)blockIdx.x * 16 + 15, R - 1),
-                                       min((int)blockIdx.y * 16 + 15, R - 1), lane);
-        if (lane == 0) s_cls = cls;
+// one record pair: both records' Eq. 1 terms with packed f32x2 arithmetic (same
+// per-element operations and rounding as the scalar form).  w = max(e - rem, 0)
+// with rem = ex2.approx(Q_CUT): the cut-off r2 >= 12.25 of rbf.py:73 is where
+// exp(-r2/2) reaches the remainder, so the clamp alone zeroes every record past it
+// (up to the ulp-level error of ex2.approx near the cut, far below the height
+// tolerance).
+__device__ __forceinline__ void pair2(Acc& A, float2 nrx, float2 nry, float2 nrem, const float4& xy,
+                                      const float4& st, const float2& dd) {
+    const float2 dx = __fadd2_rn(make_float2(xy.x, xy.y), nrx);
+    const float2 dy = __fadd2_rn(make_float2(xy.z, xy.w), nry);
+    const float2 q = __fmul2_rn(__ffma2_rn(dx, dx, __fmul2_rn(dy, dy)), make_float2(st.x, st.y));
+    const float2 e = __fadd2_rn(make_float2(ex2_approx(q.x), ex2_approx(q.y)), nrem);
+    const float2 w = make_float2(fmaxf(e.x, 0.f), fmaxf(e.y, 0.f));
+    A.w = __fadd2_rn(A.w, w);
+    A.t = __ffma2_rn(w, make_float2(st.z, st.w), A.t);
+    A.d = __ffma2_rn(w, dd, A.d);
+}
+
+// the four record pairs of a quad (QUAD float4 at q), in list order
+__device__ __forceinline__ void quad4(Acc& A, float2 nrx, float2 nry, float2 nrem, const float4* q) {
+    const float4 d01 = q[8], d23 = q[9];
+    pair2(A, nrx, nry, nrem, q[0], q[4], make_float2(d01.x, d01.y));
+    pair2(A, nrx, nry, nrem, q[1], q[5], make_float2(d01.z, d01.w));
+    pair2(A, nrx, nry, nrem, q[2], q[6], make_float2(d23.x, d23.y));
+    pair2(A, nrx, nry, nrem, q[3], q[7], make_float2(d23.z, d23.w));
+}
+__device__ __forceinline__ void quad4_global(Acc& A, float2 nrx, float2 nry, float2 nrem,
+                                             const float4* __restrict__ q) {
+    float4 v[QUAD];
+#pragma unroll
+    for (int i = 0; i < QUAD; ++i) v[i] = __ldg(q + i);
+    pair2(A, nrx, nry, nrem, v[0], v[4], make_float2(v[8].x, v[8].y));
+    pair2(A, nrx, nry, nrem, v[1], v[5], make_float2(v[8].z, v[8].w));
+    pair2(A, nrx, nry, nrem, v[2], v[6], make_float2(v[9].x, v[9].y));
+    pair2(A, nrx, nry, nrem, v[3], v[7], make_float2(v[9].z, v[9].w));
+}
+
+// One unit of 32 texels of a warp: lane -> region texel, its cell's record range,
+// and the warp's cell groups (lane t < ng holds group t's first pair and pair count).
+struct Unit {
+    int e;          // region texel index of this lane (-1: no texel)
+    int gid;        // this lane's group (-1: not a valid texel)
+    int ng;         // groups (warp-uniform)
+    int gb, gn;     // lane t < ng: group t's first record quad, quad count
+    int chg;        // record pairs per group slot per chunk (whole quads)
+    int nchunks;    // chunks of the staged path (0: per-lane gather)
+    int pb, np;     // this lane's first record quad and quad count (np = 0: invalid texel)
+    int cell;
+};
+
+template <int REG>
+__device__ __forceinline__ int unit_texel(int u, int lane) {
+    if (u < 32) return (4 * (u >> 2) + (lane >> 3)) * REG + 8 * (u & 3) + (lane & 7);   // 8x4 tiles
+    if (u == 32) return 32 * REG + lane;            // halo row (y = 32, x = 0..31)
+    if (u == 33) return lane * REG + 32;            // halo column (x = 32, y = 0..31)
+    return lane == 0 ? 32 * REG + 32 : -1;          // halo corner
+}
+
+template <int REG>
+__device__ __forceinline__ Unit plan_unit(int u, int lane, const int* s_cell, const int2* s_pr) {
+    Unit U;
+    U.e = unit_texel<REG>(u, lane);
+    U.pb = 0, U.np = 0, U.cell = -1;
+    if (U.e >= 0) {
+        const int2 pr = s_pr[U.e];
+        U.pb = pr.x >> 2;
+        U.np = ((pr.y + 1) >> 1) + 3 >> 2;
+        U.cell = s_cell[U.e];
     }
-    __syncthreads();
-    const int cls = s_cls;
-    if (cls == 0) {                        // whole block outside the mask polygon
-        if (in_raster) {
-            c.terrain[o] = P.sentinel;
-            c.water[o] = P.sentinel;
-            c.valid[o] = 0;
-            if (c.mask) c.mask[o] = 0;
-        }
-        return;
-    }
-    const double px = dadd(c.origin_x, dmul((double)ix, c.texel));
-    const double py = dadd(c.origin_y, dmul((double)iy, c.texel));
-    const bool vis = in_raster && (cls == 1 || texel_visible(c, px, py));
-    const int a = vis ? containing_cell(g, px, py) : -1;
-
-    float ter = P.sentinel, wat = P.sentinel;
-    bool zero_w = false;
-    unsigned n_pairs = 0;
-    __shared__ __align__(16) float4 s_xy[DISC_WARPS][2][STAGE_PAIRS + STAGE_GROUPS];
-    __shared__ __align__(16) float4 s_st[DISC_WARPS][2][STAGE_PAIRS + STAGE_GROUPS];
-    __shared__ __align__(16) float2 s_d[DISC_WARPS][2][STAGE_PAIRS + STAGE_GROUPS];
-
-    // distinct cells of the warp (up to STAGE_GROUPS): lane t < ng holds group t's pair range
     const unsigned FULL = 0xffffffffu;
-    unsigned rem = __ballot_sync(FULL, a >= 0);
-    const bool any_valid = rem != 0u;
-    int gid = -1, ng = 0, g_beg = 0, g_end = 0;
+    unsigned rem = __ballot_sync(FULL, U.np > 0);
+    U.gid = -1, U.ng = 0, U.gb = 0, U.gn = 0;
 #pragma unroll
     for (int t = 0; t < STAGE_GROUPS; ++t) {
         if (rem) {
-            const int cell = __shfl_sync(FULL, a, __ffs(rem) - 1);
-            const unsigned m = __ballot_sync(FULL, a == cell);
-            if (a == cell) gid = t;
-            if (lane == t) {
-                g_beg = __ldg(g.pair_offsets + cell);
-                g_end = __ldg(g.pair_offsets + cell + 1);
-            }
+            const int src = __ffs(rem) - 1;
+            const int key = __shfl_sync(FULL, U.pb, src);
+            const int kn = __shfl_sync(FULL, U.np, src);
+            const bool mine = U.np > 0 && U.pb == key;
+            const unsigned m = __ballot_sync(FULL, mine);
+            if (mine) U.gid = t;
+            if (lane == t) U.gb = key, U.gn = kn;
             rem &= ~m;
-            ng = t + 1;
+            U.ng = t + 1;
         }
     }
-    const bool staged = any_valid && rem == 0u;
-
-    float wsum = 0.f, tn = 0.f, dn = 0.f;
-#ifdef DISC_PACKED_SUMS
-    float2 ws2 = make_float2(0.f, 0.f), tn2 = ws2, dn2 = ws2;
-#endif
-    float2 nrel = make_float2(0.f, 0.f), nrely = make_float2(0.f, 0.f);
-    if (a >= 0) {
-        const float relx = (float)dsub(px, g.cx[a]);
-        const float rely = (float)dsub(py, g.cy[a]);
-        nrel = make_float2(-relx, -relx);
-        nrely = make_float2(-rely, -rely);
-        n_pairs = (unsigned)(__ldg(g.offsets + a + 1) - __ldg(g.offsets + a));
+    U.chg = 0;
+    U.nchunks = 0;
+    if (U.ng > 0 && rem == 0u) {
+        U.chg = group_chunk(U.ng);
+        const int maxq = (int)__reduce_max_sync(FULL, (unsigned)(lane < U.ng ? U.gn : 0));
+        const int cq = U.chg >> 2;
+        U.nchunks = (maxq + cq - 1) / cq;
     }
-    // one record pair: the two records' Eq. 1 terms with packed f32x2 arithmetic
-    // (same per-element operations and rounding as the scalar form), then the
-    // sums in list order
-    auto pair2 = [&](const float4& xy, const float4& st, const float2& dd) {
-        const float2 dx = __fadd2_rn(make_float2(xy.x, xy.y), nrel);
-        const float2 dy = __fadd2_rn(make_float2(xy.z, xy.w), nrely);
-        const float2 q = __fmul2_rn(__ffma2_rn(dx, dx, __fmul2_rn(dy, dy)), make_float2(st.x, st.y));
-        const float e0 = ex2_approx(q.x) - REMAINDER_F, e1 = ex2_approx(q.y) - REMAINDER_F;
-        const float w0 = (q.x > Q_CUT) ? fmaxf(e0, 0.f) : 0.f;
-        const float w1 = (q.y > Q_CUT) ? fmaxf(e1, 0.f) : 0.f;
-#ifdef DISC_PACKED_SUMS
-        const float2 w = make_float2(w0, w1);
-        ws2 = __fadd2_rn(ws2, w);
-        tn2 = __ffma2_rn(w, make_float2(st.z, st.w), tn2);
-        dn2 = __ffma2_rn(w, dd, dn2);
-#else
-        wsum += w0;
-        wsum += w1;
-        tn = fmaf(w0, st.z, tn);
-        tn = fmaf(w1, st.w, tn);
-        dn = fmaf(w0, dd.x, dn);
-        dn = fmaf(w1, dd.y, dn);
-#endif
-    };
-    const float4* __restrict__ gxy = reinterpret_cast<const float4*>(g.rec_xy);
-    const float4* __restrict__ gst = reinterpret_cast<const float4*>(g.rec_st);
-    const float2* __restrict__ gd = reinterpret_cast<const float2*>(g.rec_d);
-    if (staged) {
-        // group slots of chg pairs (+1 pad: groups start in different banks)
-        const int lg = 6 - (32 - __clz(ng - 1));      // 64 / next_pow2(ng) pairs per group
-        const int chg = 1 << lg;
-        const int maxlen = __reduce_max_sync(FULL, (unsigned)(lane < ng ? g_end - g_beg : 0));
-        const int nchunks = (maxlen + chg - 1) >> lg;
-        auto issue = [&](int k, int buf) {
-#pragma unroll
-            for (int i = 0; i < STAGE_PAIRS / 32; ++i) {
-                const int r = i * 32 + lane;
-                const int gg = r >> lg, idx = r & (chg - 1);
-                const int gb = __shfl_sync(FULL, g_beg, gg), ge = __shfl_sync(FULL, g_end, gg);
-                const int src = gb + (k << lg) + idx;
-                if (gg < ng && src < ge) {
-                    const int dst = gg * (chg + 1) + idx;
-                    cp_async16(&s_xy[warp][buf][dst], gxy + src);
-                    cp_async16(&s_st[warp][buf][dst], gst + src);
-                    cp_async8(&s_d[warp][buf][dst], gd + src);
+    return U;
+}
+
+template <bool MIPS>
+__global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_constant__ DiscParams P,
+                                                       const __grid_constant__ HcGrid g) {
+    constexpr int REG = MIPS ? BLK + 1 : BLK;      // region side (block + halo)
+    constexpr int NT = REG * REG;
+    constexpr int NU = MIPS ? 35 : 32;             // units of 32 texels
+    const unsigned FULL = 0xffffffffu;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    if ((int)blockIdx.x >= P.n_blocks) {           // tile-queue order: one histogram chunk per CTA
+        const int chunk = (int)blockIdx.x - P.n_blocks;
+        if (chunk < order_chunks(P.ord.n_tiles)) order_count_chunk<256>(P.ord.cost, P.ord.order, P.ord.n_tiles, chunk);
+        return;
+    }
+    const int bs = P.blocks_side;
+    // far cascades first: their blocks are the heaviest (many small cells per block,
+    // per-lane gathers), so the light near-cascade blocks fill the tail
+    const int kc = P.n_cascades - 1 - (int)blockIdx.x / (bs * bs);
+    const int rb = (int)blockIdx.x % (bs * bs);
+    const HcCascadeRaster& c = P.c[kc];
+    const int R = c.resolution, n0 = R - 1;
+    const int bx = (rb % bs) * BLK, by = (rb / bs) * BLK;
+    if (bx >= R || by >= R) return;
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    int* s_cell = reinterpret_cast<int*>(smem);                                    // [NT]
+    int2* s_pr = reinterpret_cast<int2*>(smem + 4 * ((NT + 1) & ~1));             // [NT] {first pair, list length}
+    float2* s_rv = reinterpret_cast<float2*>(s_pr + NT);                           // [NT] offset to cell -> {terrain, water}
+    uint8_t* s_flag = reinterpret_cast<uint8_t*>(s_rv + NT);                       // [NT] 1 mask, 2 valid, 4 in raster, 8 layers differ
+    unsigned char* s_stage = smem + (((size_t)(4 * ((NT + 1) & ~1) + 16 * NT + NT) + 127) & ~(size_t)127);
+    float4* s_q = reinterpret_cast<float4*>(s_stage);                             // [W][2][STAGE_F4]
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_q + DISC_WARPS * 2 * STAGE_F4); // [W][2]
+    __shared__ int s_cls, s_next;
+    __shared__ float s_red[2][2][DISC_WARPS];
+
+    if (warp == 0) {
+        const int x1 = min(bx + REG - 1, R - 1), y1 = min(by + REG - 1, R - 1);
+        const int cls = classify_block(c, bx, by, x1, y1, lane);
+        if (lane == 0) {
+            s_cls = cls;
+            s_next = 0;
+        }
+    }
+    if (tid < 2 * DISC_WARPS) mbar_init(&s_bar[tid], 1);
+    __syncthreads();
+    const int cls = s_cls;
+    const float sentinel = P.sentinel;
+
+    // whole rows of 4 texels per thread when rows are 16-byte aligned
+    const bool vec4 = (R & 3) == 0 && bx + BLK <= R;
+    if (cls == 0) {        // the whole region lies outside the mask polygon
+        if (vec4) {
+            const int y = by + (tid >> 3), x = bx + 4 * (tid & 7);
+            if (y < R) {
+                const int64_t o = (int64_t)y * R + x;
+                const float4 sv = make_float4(sentinel, sentinel, sentinel, sentinel);
+                *reinterpret_cast<float4*>(c.terrain + o) = sv;
+                *reinterpret_cast<float4*>(c.water + o) = sv;
+                *reinterpret_cast<uint32_t*>(c.valid + o) = 0u;
+                if (c.mask) *reinterpret_cast<uint32_t*>(c.mask + o) = 0u;
+            }
+        } else {
+            for (int e = tid; e < BLK * BLK; e += 256) {
+                const int x = bx + (e & 31), y = by + (e >> 5);
+                if (x < R && y < R) {
+                    const int64_t o = (int64_t)y * R + x;
+                    c.terrain[o] = sentinel;
+                    c.water[o] = sentinel;
+                    c.valid[o] = 0;
+                    if (c.mask) c.mask[o] = 0;
                 }
             }
-            cp_async_commit();
-        };
-        const int gsel = gid >= 0 ? gid : 0;
-        const int mb = __shfl_sync(FULL, g_beg, gsel), me = __shfl_sync(FULL, g_end, gsel);
-        const int mylen = gid >= 0 ? me - mb : 0;
-        const int myoff = gsel * (chg + 1);
-        issue(0, 0);
-        for (int k = 0; k < nchunks; ++k) {
-            if (k + 1 < nchunks) {
-                issue(k + 1, (k + 1) & 1);
-                cp_async_wait<1>();
-            } else {
-                cp_async_wait<0>();
-            }
-            __syncwarp();
-            const float4* XY = &s_xy[warp][k & 1][myoff];
-            const float4* ST = &s_st[warp][k & 1][myoff];
-            const float2* D = &s_d[warp][k & 1][myoff];
-            const int n = min(chg, mylen - (k << lg));
-            int u = 0;
-            for (; u + 4 <= n; u += 4) {
-#pragma unroll
-                for (int v = 0; v < 4; ++v) pair2(XY[u + v], ST[u + v], D[u + v]);
-            }
-            for (; u < n; ++u) pair2(XY[u], ST[u], D[u]);
-            __syncwarp();                  // buffer k & 1 is refilled at step k + 1
         }
-    } else if (a >= 0) {
-        const int beg = __ldg(g.pair_offsets + a), end = __ldg(g.pair_offsets + a + 1);
-#ifndef DISC_NO_L2_PREFETCH
-        // lanes of this path walk different lists: start streaming each whole list into
-        // L2 at once so the batched loads below wait for L2 rather than DRAM
-        prefetch_l2(gxy + beg, (end - beg) * 16);
-        prefetch_l2(gst + beg, (end - beg) * 16);
-        prefetch_l2(gd + beg, (end - beg) * 8);
-#endif
-        // batches of DISC_BATCH pairs: all loads issued before the (in-order) accumulation
-        int j = beg;
-        for (; j + DISC_BATCH <= end; j += DISC_BATCH) {
-            float4 xy[DISC_BATCH], st[DISC_BATCH];
-            float2 dd[DISC_BATCH];
-#pragma unroll
-            for (int u = 0; u < DISC_BATCH; ++u) {
-                xy[u] = __ldg(gxy + j + u);
-                st[u] = __ldg(gst + j + u);
-                dd[u] = __ldg(gd + j + u);
+        if (MIPS) {
+            // The block's top node (level 5, or the pyramid top for small rasters) is the
+            // sentinel, below every ray height of the traversal slab [hmin, hmax]
+            // (hmin >= h_lo - float rounding > sentinel = h_lo - 1), so the traversal
+            // steps over it and never reads the block's lower levels or patch bytes
+            // (_kernels.py:134-166).  They are written only when the caller inspects the
+            // whole pyramid (debug frames).
+            const int L0 = P.full_mips ? 0 : min(TILE_LEVELS, P.n_levels) - 1;
+            for (int L = L0; L < TILE_LEVELS && L < P.n_levels; ++L) {
+                const int side = BLK >> L, wl = P.level_w[L];
+                for (int e = tid; e < side * side; e += 256) {
+                    const int gx = (bx >> L) + e % side, gy = (by >> L) + e / side;
+                    if (gx < wl && gy < wl) {
+                        const int64_t o = P.level_off[L] + (int64_t)gy * wl + gx;
+                        P.mip[kc][0][o] = sentinel;
+                        P.mip[kc][1][o] = sentinel;
+                        if (L == 0 && P.patch_ok[kc]) P.patch_ok[kc][(int64_t)gy * n0 + gx] = 0;
+                    }
+                }
             }
-#pragma unroll
-            for (int u = 0; u < DISC_BATCH; ++u) pair2(xy[u], st[u], dd[u]);
+            if (tid < 2) {
+                float* pp = P.partial + ((int64_t)(2 * kc + tid) * P.max_tiles + rb) * 2;
+                pp[0] = INFINITY;
+                pp[1] = -INFINITY;
+            }
         }
-        for (; j < end; ++j) pair2(__ldg(gxy + j), __ldg(gst + j), __ldg(gd + j));
+        return;
     }
-#ifdef DISC_PACKED_SUMS
-    wsum = ws2.x + ws2.y;
-    tn = tn2.x + tn2.y;
-    dn = dn2.x + dn2.y;
-#endif
-    if (a >= 0) {
-        zero_w = !(wsum > 0.f);
-        const float inv = 1.0f / wsum;
-        ter = __ldg(g.anchor_t + a) + tn * inv;
-        const float dep = fmaxf(__ldg(g.anchor_d + a) + dn * inv, 0.f);
-        wat = ter + dep;
+
+    // ---- 2. per-texel mask, cell lookup and record range (all dependent loads here)
+    {
+        constexpr int PER = (NT + 255) / 256;
+        int cell[PER];
+        double pxs[PER], pys[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = tid + 256 * i;
+            cell[i] = -1;
+            pxs[i] = pys[i] = 0.0;
+            if (e < NT) {
+                const int x = bx + e % REG, y = by + e / REG;
+                const bool inr = x < R && y < R;
+                const double px = dadd(c.origin_x, dmul((double)x, c.texel));
+                const double py = dadd(c.origin_y, dmul((double)y, c.texel));
+                const bool vis = inr && (cls == 1 || texel_visible(c, px, py));
+                if (vis) cell[i] = containing_cell(g, px, py);
+                pxs[i] = px, pys[i] = py;
+                s_flag[e] = (uint8_t)((vis ? 1 : 0) | (inr ? 4 : 0));
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = tid + 256 * i;
+            if (e < NT) {
+                const int a = cell[i];
+                int2 pr = make_int2(0, 0);
+                float2 rel = make_float2(0.f, 0.f);
+                if (a >= 0) {
+                    pr.x = __ldg(g.pair_offsets + a);
+                    pr.y = __ldg(g.offsets + a + 1) - __ldg(g.offsets + a);
+                    rel.x = (float)dsub(pxs[i], __ldg(g.cx + a));
+                    rel.y = (float)dsub(pys[i], __ldg(g.cy + a));
+                }
+                s_cell[e] = a;
+                s_pr[e] = pr;
+                s_rv[e] = rel;
+            }
+        }
     }
-    if (in_raster) {
-        c.terrain[o] = ter;
-        c.water[o] = wat;
-        c.valid[o] = a >= 0;
-        if (c.mask) c.mask[o] = vis;
+    __syncthreads();
+    // unit order: longest first (a unit takes as long as its longest list), so the
+    // warps of the block finish together (longest-processing-time scheduling)
+    __shared__ int s_ucost[NU];
+    __shared__ int s_uorder[NU];
+    for (int v = warp; v < NU; v += DISC_WARPS) {
+        const int e = unit_texel<REG>(v, lane);
+        const unsigned q = e >= 0 ? (unsigned)((((s_pr[e].y + 1) >> 1) + 3) >> 2) : 0u;
+        const unsigned m = __reduce_max_sync(FULL, q);
+        if (lane == 0) s_ucost[v] = (int)m;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        for (int v = lane; v < NU; v += 32) {
+            const int cv = s_ucost[v];
+            int rank = 0;
+            for (int w = 0; w < NU; ++w) {
+                const int cw = s_ucost[w];
+                rank += (cw > cv) || (cw == cv && w < v);
+            }
+            s_uorder[rank] = v;
+        }
+    }
+    __syncthreads();
+
+    // ---- 3. units: staged (TMA bulk copies into a per-warp double buffer) or gathered
+    const float rem = ex2_approx(Q_CUT);
+    const float2 nrem = make_float2(-rem, -rem);
+    float4* const wq = s_q + warp * 2 * STAGE_F4;
+    uint64_t* const wbar = s_bar + warp * 2;
+    const float4* __restrict__ grec = reinterpret_cast<const float4*>(g.rec);
+    unsigned phase = 0u;       // bit b: parity of buffer b's next completion
+    int buf = 0;               // buffer of the next chunk to consume
+
+    // copy chunk k of unit U's groups into buffer b (every lane calls; lane t < ng
+    // copies group t's quads [k * cq, min((k + 1) * cq, gn)) -- one bulk copy)
+    auto issue = [&](const Unit& U, int k, int b) {
+        const int cq = U.chg >> 2;
+        int n = 0;
+        if (lane < U.ng) n = min(cq, U.gn - k * cq);
+        n = n > 0 ? n : 0;
+        const unsigned bytes = (unsigned)__reduce_add_sync(FULL, (unsigned)(16 * QUAD * n));
+        if (lane == 0) mbar_expect_tx(&wbar[b], bytes);
+        __syncwarp();
+        if (n > 0) {
+            fence_proxy_async();
+            bulk_g2s(&wq[b * STAGE_F4 + lane * (cq * QUAD + 1)], grec + (int64_t)(U.gb + k * cq) * QUAD,
+                     16u * QUAD * n, &wbar[b]);
+        }
+    };
+    auto grab = [&]() {
+        int u = 0;
+        if (lane == 0) {
+            u = atomicAdd(&s_next, 1);
+            u = u < NU ? s_uorder[u] : NU;
+        }
+        return __shfl_sync(FULL, u, 0);
+    };
+
+    bool zero_w = false;
+    int u = grab();
+    Unit U;
+    if (u < NU) {
+        U = plan_unit<REG>(u, lane, s_cell, s_pr);
+        if (U.nchunks) issue(U, 0, buf);
+    }
+    while (u < NU) {
+        const int un = grab();
+        Unit N;
+        N.nchunks = 0;
+        if (un < NU) N = plan_unit<REG>(un, lane, s_cell, s_pr);
+        // lane's texel: anchors (consumed after the records) and offset to its cell centre
+        float at = 0.f, ad = 0.f;
+        float2 nrx = make_float2(0.f, 0.f), nry = nrx;
+        if (U.np > 0) {
+            at = __ldg(g.anchor_t + U.cell);
+            ad = __ldg(g.anchor_d + U.cell);
+            const float2 rel = s_rv[U.e];
+            nrx = make_float2(-rel.x, -rel.x);
+            nry = make_float2(-rel.y, -rel.y);
+        }
+        Acc A;
+        A.w = A.t = A.d = make_float2(0.f, 0.f);
+        if (U.nchunks) {
+            const int cq = U.chg >> 2;
+            const int myoff = (U.gid >= 0 ? U.gid : 0) * (cq * QUAD + 1);
+            for (int k = 0; k < U.nchunks; ++k) {
+                // keep one chunk in flight: this unit's next, else the next unit's first
+                if (k + 1 < U.nchunks) issue(U, k + 1, buf ^ 1);
+                else if (N.nchunks) issue(N, 0, buf ^ 1);
+                mbar_wait(&wbar[buf], (phase >> buf) & 1u);
+                phase ^= 1u << buf;
+                const float4* Q = &wq[buf * STAGE_F4 + myoff];
+                const int n = U.gid >= 0 ? min(cq, U.np - k * cq) : 0;
+                for (int v = 0; v < n; ++v) quad4(A, nrx, nry, nrem, Q + v * QUAD);
+                __syncwarp();              // buffer `buf` is refilled by a later issue
+                buf ^= 1;
+            }
+        } else {
+            if (N.nchunks) issue(N, 0, buf);     // buffers are idle during a gathered unit
+            if (U.np > 0) {
+                // lanes walk different lists: stream each whole list into L2 at once so
+                // the loads below wait for L2 rather than DRAM
+                const float4* q = grec + (int64_t)U.pb * QUAD;
+                prefetch_l2(q, U.np * 16 * QUAD);
+                for (int v = 0; v < U.np; ++v) quad4_global(A, nrx, nry, nrem, q + v * QUAD);
+            }
+        }
+        // Eq. 2 (rbf.py:119-129): anchored sums, depth clamp, water = terrain + depth
+        if (U.e >= 0) {
+            const uint8_t f = s_flag[U.e];
+            float ter = (f & 4) ? sentinel : -INFINITY, wat = ter;    // -inf: outside the raster (mips)
+            uint8_t nf = f;
+            if (U.np > 0) {
+                const float wsum = A.w.x + A.w.y;
+                zero_w |= !(wsum > 0.f);
+                const float inv = 1.0f / wsum;
+                ter = at + (A.t.x + A.t.y) * inv;
+                const float dep = fmaxf(ad + (A.d.x + A.d.y) * inv, 0.f);
+                wat = ter + dep;
+                nf |= 2;
+            }
+            if (__float_as_uint(ter) != __float_as_uint(wat)) nf |= 8;
+            s_rv[U.e] = make_float2(ter, wat);
+            s_flag[U.e] = nf;
+        }
+        u = un;
+        U = N;
+    }
+    __syncthreads();
+
+    // ---- 4. epilogue: owned texels, counters, mips 0..5, patch bytes, valid range
+    float vmin0 = INFINITY, vmax0 = -INFINITY, vmin1 = INFINITY, vmax1 = -INFINITY;
+    unsigned nvis = 0, nval = 0;
+    unsigned long long npairs = 0;
+    auto tally = [&](const float2& h, uint8_t f, int r) {
+        nvis += f & 1;
+        if (f & 2) {
+            ++nval;
+            npairs += (unsigned)s_pr[r].y;
+            vmin0 = fminf(vmin0, h.x), vmax0 = fmaxf(vmax0, h.x);
+            vmin1 = fminf(vmin1, h.y), vmax1 = fmaxf(vmax1, h.y);
+        }
+    };
+    if (vec4) {
+        const int ty = tid >> 3, tx = 4 * (tid & 7);
+        const int y = by + ty;
+        if (y < R) {
+            const int r = ty * REG + tx;
+            float2 h[4];
+            uint8_t f[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                h[i] = s_rv[r + i];
+                f[i] = s_flag[r + i];
+                tally(h[i], f[i], r + i);
+            }
+            const int64_t o = (int64_t)y * R + bx + tx;
+            *reinterpret_cast<float4*>(c.terrain + o) = make_float4(h[0].x, h[1].x, h[2].x, h[3].x);
+            *reinterpret_cast<float4*>(c.water + o) = make_float4(h[0].y, h[1].y, h[2].y, h[3].y);
+            *reinterpret_cast<uint32_t*>(c.valid + o) =
+                ((f[0] >> 1) & 1u) | (((f[1] >> 1) & 1u) << 8) | (((f[2] >> 1) & 1u) << 16) | (((f[3] >> 1) & 1u) << 24);
+            if (c.mask)
+                *reinterpret_cast<uint32_t*>(c.mask + o) =
+                    (f[0] & 1u) | ((f[1] & 1u) << 8) | ((f[2] & 1u) << 16) | ((f[3] & 1u) << 24);
+        }
+    } else {
+        for (int e = tid; e < BLK * BLK; e += 256) {
+            const int tx = e & 31, ty = e >> 5;
+            const int x = bx + tx, y = by + ty;
+            if (x < R && y < R) {
+                const int r = ty * REG + tx;
+                const float2 h = s_rv[r];
+                const uint8_t f = s_flag[r];
+                const int64_t o = (int64_t)y * R + x;
+                c.terrain[o] = h.x;
+                c.water[o] = h.y;
+                c.valid[o] = (f >> 1) & 1;
+                if (c.mask) c.mask[o] = f & 1;
+                tally(h, f, r);
+            }
+        }
     }
     if (P.counters) {
-        const unsigned nvis = __popc(__ballot_sync(0xffffffffu, vis));
-        const unsigned nval = __popc(__ballot_sync(0xffffffffu, a >= 0));
-        const bool anyzero = __any_sync(0xffffffffu, zero_w);
-        unsigned pairs = n_pairs;
+        nvis = __reduce_add_sync(FULL, nvis);
+        nval = __reduce_add_sync(FULL, nval);
 #pragma unroll
-        for (int s = 16; s > 0; s >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, s);
+        for (int s = 16; s > 0; s >>= 1) npairs += __shfl_xor_sync(FULL, npairs, s);
+        const bool anyzero = __any_sync(FULL, zero_w);
         if (lane == 0) {
             if (nvis) atomicAdd(P.counters + HC_CNT_VISIBLE, (unsigned long long)nvis);
             if (nval) atomicAdd(P.counters + HC_CNT_VALID, (unsigned long long)nval);
             if (anyzero) atomicOr(P.counters + HC_CNT_ZERO_WEIGHT, 1ull);
-            if (pairs) atomicAdd(P.counters + HC_CNT_PAIRS, (unsigned long long)pairs);
+            if (npairs) atomicAdd(P.counters + HC_CNT_PAIRS, npairs);
         }
     }
+    if (!MIPS) return;
+
+    // level 0 (max of each patch's four corners, raycast.py:71-76) + patch bytes
+    float* lv = reinterpret_cast<float*>(s_stage);             // [2][BLK][BLK + 1] (the staging area is idle)
+    for (int e = tid; e < BLK * BLK; e += 256) {
+        const int tx = e & 31, ty = e >> 5;
+        const int gx = bx + tx, gy = by + ty;
+        float m0 = -INFINITY, m1 = -INFINITY;
+        if (gx < n0 && gy < n0) {
+            const int r = ty * REG + tx;
+            const float2 a = s_rv[r], b = s_rv[r + 1], cc = s_rv[r + REG], d = s_rv[r + REG + 1];
+            m0 = fmaxf(fmaxf(a.x, b.x), fmaxf(cc.x, d.x));
+            m1 = fmaxf(fmaxf(a.y, b.y), fmaxf(cc.y, d.y));
+            const int64_t o = (int64_t)gy * n0 + gx;
+            P.mip[kc][0][o] = m0;
+            P.mip[kc][1][o] = m1;
+            if (P.patch_ok[kc]) {
+                const uint8_t fa = s_flag[r], fb = s_flag[r + 1], fc = s_flag[r + REG], fd = s_flag[r + REG + 1];
+                P.patch_ok[kc][o] = (uint8_t)(((fa & fb & fc & fd) >> 1 & 1) | (((fa | fb | fc | fd) >> 2) & 2));
+            }
+        }
+        lv[ty * (BLK + 1) + tx] = m0;
+        lv[BLK * (BLK + 1) + ty * (BLK + 1) + tx] = m1;
+    }
+    __syncthreads();
+    // levels 1..5 in place: after level L, lv[.][y][x] for y, x < BLK >> L holds level L
+    for (int L = 1; L < TILE_LEVELS && L < P.n_levels; ++L) {
+        const int side = BLK >> L;
+        const int wl = P.level_w[L];
+        float m0 = 0.f, m1 = 0.f;
+        int y = 0, x = 0;
+        if (tid < side * side) {
+            y = tid / side;
+            x = tid % side;
+            const float* l0 = lv;
+            const float* l1 = lv + BLK * (BLK + 1);
+            const int s = BLK + 1;
+            m0 = fmaxf(fmaxf(l0[2 * y * s + 2 * x], l0[2 * y * s + 2 * x + 1]),
+                       fmaxf(l0[(2 * y + 1) * s + 2 * x], l0[(2 * y + 1) * s + 2 * x + 1]));
+            m1 = fmaxf(fmaxf(l1[2 * y * s + 2 * x], l1[2 * y * s + 2 * x + 1]),
+                       fmaxf(l1[(2 * y + 1) * s + 2 * x], l1[(2 * y + 1) * s + 2 * x + 1]));
+        }
+        __syncthreads();
+        if (tid < side * side) {
+            lv[y * (BLK + 1) + x] = m0;
+            lv[BLK * (BLK + 1) + y * (BLK + 1) + x] = m1;
+            const int gy = (by >> L) + y, gx = (bx >> L) + x;
+            if (gx < wl && gy < wl) {
+                const int64_t o = P.level_off[L] + (int64_t)gy * wl + gx;
+                P.mip[kc][0][o] = m0;
+                P.mip[kc][1][o] = m1;
+            }
+        }
+        __syncthreads();
+    }
+    // block partial min/max of valid heights, per layer (every texel counted by its owner)
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        vmin0 = fminf(vmin0, __shfl_xor_sync(FULL, vmin0, s));
+        vmax0 = fmaxf(vmax0, __shfl_xor_sync(FULL, vmax0, s));
+        vmin1 = fminf(vmin1, __shfl_xor_sync(FULL, vmin1, s));
+        vmax1 = fmaxf(vmax1, __shfl_xor_sync(FULL, vmax1, s));
+    }
+    if (lane == 0) {
+        s_red[0][0][warp] = vmin0, s_red[0][1][warp] = vmax0;
+        s_red[1][0][warp] = vmin1, s_red[1][1][warp] = vmax1;
+    }
+    __syncthreads();
+    if (tid < 2) {
+        float a = s_red[tid][0][0], b = s_red[tid][1][0];
+        for (int w = 1; w < DISC_WARPS; ++w) {
+            a = fminf(a, s_red[tid][0][w]);
+            b = fmaxf(b, s_red[tid][1][w]);
+        }
+        float* pp = P.partial + ((int64_t)(2 * kc + tid) * P.max_tiles + rb) * 2;
+        pp[0] = a;
+        pp[1] = b;
+    }
 }
+
+template <bool MIPS>
+constexpr size_t disc_smem_bytes() {
+    constexpr size_t REG = MIPS ? BLK + 1 : BLK;
+    constexpr size_t NT = REG * REG;
+    constexpr size_t head = ((4 * ((NT + 1) & ~(size_t)1) + 16 * NT + NT) + 127) & ~(size_t)127;
+    constexpr size_t stage = DISC_WARPS * 2 * 16 * STAGE_F4 + DISC_WARPS * 2 * 8;
+    return head + stage;
+}
+static_assert(DISC_WARPS * 2 * 16 * STAGE_F4 >= 2 * BLK * (BLK + 1) * 4, "mip levels alias the staging area");
+constexpr bool stage_fits() {
+    for (int ng = 1; ng <= STAGE_GROUPS; ++ng)
+        if (ng * (group_chunk(ng) / 4 * QUAD + 1) > STAGE_F4 || group_chunk(ng) < 4) return false;
+    return true;
+}
+static_assert(stage_fits(), "a chunk of STAGE_GROUPS groups overflows the warp buffer");
 
 // float64 Eq. 2 at arbitrary points (rbf.py:87-130 per segment)
 __global__ void k_eval_points(HcGrid g, const double* __restrict__ px, const double* __restrict__ py,
@@ -454,16 +842,16 @@ __global__ void k_eval_points(HcGrid g, const double* __restrict__ px, const dou
 
 using namespace hc;
 
-extern "C" int hc_build_records(const HcGrid* grid, float* rec_xy, float* rec_st, float* rec_d, float* anchor_t,
-                                float* anchor_d, hc_stream_t stream) {
-    HC_REQUIRE(grid && rec_xy && rec_st && rec_d && anchor_t && anchor_d, "hc_build_records: null argument");
+extern "C" int hc_build_records(const HcGrid* grid, float* rec, float* anchor_t, float* anchor_d,
+                                hc_stream_t stream) {
+    HC_REQUIRE(grid && rec && anchor_t && anchor_d, "hc_build_records: null argument");
+    HC_REQUIRE((uintptr_t)rec % 16 == 0, "hc_build_records: records must be 16-byte aligned");
     HC_REQUIRE(grid->offsets && grid->indices && grid->pair_offsets, "hc_build_records: grid without CSR");
     HC_REQUIRE(grid->n_cells >= 0, "hc_build_records: negative cell count");
     if (grid->n_cells == 0) return HC_OK;
     const int blocks = (int)(((int64_t)grid->n_cells * 32 + 255) / 256);
     k_build_records<<<blocks, 256, 0, (cudaStream_t)stream>>>(
-        *grid, reinterpret_cast<float4*>(rec_xy), reinterpret_cast<float4*>(rec_st),
-        reinterpret_cast<float2*>(rec_d), anchor_t, anchor_d);
+        *grid, reinterpret_cast<float4*>(rec), anchor_t, anchor_d);
     return cuda_status("hc_build_records");
 }
 
@@ -477,13 +865,16 @@ extern "C" int hc_visibility_mask(const HcCascadeRaster* c, hc_stream_t stream) 
     return cuda_status("hc_visibility_mask");
 }
 
-extern "C" int hc_discretize(const HcCascadeRaster* cascades, int n_cascades, const HcGrid* grid,
-                             float sentinel, uint64_t* counters, hc_stream_t stream) {
+// Shared by hc_discretize (rasters only) and the frame launch (rasters + mips 0..5 +
+// patch bytes + valid-range partials + the render's tile-queue histograms).
+int hc::discretize_launch(const HcCascadeRaster* cascades, int n_cascades, const HcGrid* grid, float sentinel,
+                          uint64_t* counters, const DiscMipJob* mips, const OrderJob* ord, cudaStream_t stream) {
     HC_REQUIRE(cascades && grid, "hc_discretize: null argument");
     HC_REQUIRE(n_cascades >= 0 && n_cascades <= HC_MAX_CASCADES, "hc_discretize: %d cascades (max %d)",
                n_cascades, HC_MAX_CASCADES);
     if (n_cascades == 0) return HC_OK;
-    DiscretizeParams P;
+    DiscParams P;
+    memset(&P, 0, sizeof(P));
     int rmax = 0;
     for (int k = 0; k < n_cascades; ++k) {
         const HcCascadeRaster& c = cascades[k];
@@ -494,15 +885,66 @@ extern "C" int hc_discretize(const HcCascadeRaster* cascades, int n_cascades, co
         P.c[k] = c;
         rmax = c.resolution > rmax ? c.resolution : rmax;
     }
-    HC_REQUIRE(grid->rec_xy && grid->rec_st && grid->rec_d && grid->pair_offsets && grid->offsets &&
-                   grid->tile_index,
+    HC_REQUIRE(grid->rec && grid->pair_offsets && grid->offsets && grid->tile_index && grid->anchor_t &&
+                   grid->anchor_d,
                "hc_discretize: grid records not built");
+    HC_REQUIRE((uintptr_t)grid->rec % 16 == 0, "hc_discretize: records must be 16-byte aligned");
     P.n_cascades = n_cascades;
     P.sentinel = sentinel;
     P.counters = (unsigned long long*)counters;
-    dim3 g((rmax + 15) / 16, (rmax + 15) / 16, n_cascades);
-    k_discretize<<<g, 256, 0, (cudaStream_t)stream>>>(P, *grid);
+    P.blocks_side = (rmax + BLK - 1) / BLK;
+    P.n_blocks = n_cascades * P.blocks_side * P.blocks_side;
+    int order_ctas = 0;
+    if (mips) {
+        for (int k = 0; k < n_cascades; ++k) {
+            HC_REQUIRE(cascades[k].resolution == rmax, "hc_discretize: fused mips need equal resolutions");
+            HC_REQUIRE(mips->mip[k][0] && mips->mip[k][1], "hc_discretize: cascade %d has no mip buffers", k);
+            P.mip[k][0] = mips->mip[k][0];
+            P.mip[k][1] = mips->mip[k][1];
+            P.patch_ok[k] = mips->patch_ok[k];
+        }
+        HC_REQUIRE(mips->partial && mips->partial_slots >= P.blocks_side * P.blocks_side,
+                   "hc_discretize: partial workspace holds %d blocks, need %d", mips->partial_slots,
+                   P.blocks_side * P.blocks_side);
+        P.n_levels = mips->n_levels;
+        P.max_tiles = mips->partial_slots;
+        for (int L = 0; L < TILE_LEVELS; ++L) {
+            P.level_off[L] = mips->level_off[L];
+            P.level_w[L] = mips->level_w[L];
+        }
+        P.partial = mips->partial;
+        P.full_mips = mips->full;
+        if (ord && ord->n_tiles > 0) {
+            HC_REQUIRE(ord->cost && ord->order && ord->counter, "hc_discretize: order job with null pointers");
+            P.ord = *ord;
+            order_ctas = order_chunks(ord->n_tiles);
+        }
+    }
+    const int ctas = P.n_blocks + order_ctas;
+    if (mips) {
+        constexpr size_t smem = disc_smem_bytes<true>();
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_discretize<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = true;
+        }
+        k_discretize<true><<<ctas, 256, smem, stream>>>(P, *grid);
+    } else {
+        constexpr size_t smem = disc_smem_bytes<false>();
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_discretize<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = true;
+        }
+        k_discretize<false><<<ctas, 256, smem, stream>>>(P, *grid);
+    }
     return cuda_status("hc_discretize");
+}
+
+extern "C" int hc_discretize(const HcCascadeRaster* cascades, int n_cascades, const HcGrid* grid,
+                             float sentinel, uint64_t* counters, hc_stream_t stream) {
+    return hc::discretize_launch(cascades, n_cascades, grid, sentinel, counters, nullptr, nullptr,
+                                 (cudaStream_t)stream);
 }
 
 extern "C" int hc_eval_points(const HcGrid* grid, const double* px, const double* py,

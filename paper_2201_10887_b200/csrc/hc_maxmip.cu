@@ -38,6 +38,7 @@ struct MipParams {
     int32_t max_tiles;
     int32_t tiles_grid;             // k_mip_tiles: mip CTAs per grid row (columns past it count the order)
     int32_t n_jobs;                 // k_mip_top: CTAs past n_jobs scatter the order
+    int32_t part_side;              // k_mip_top: partials per side (0: (R - 1 + 31) / 32, k_mip_tiles')
     OrderJob ord;                   // tile-queue order of the frame's k_render (n_tiles 0: none)
 };
 
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(1024) k_mip_top(const __grid_constant__ MipPar
     }
     const HcMipJob& J = P.j[blockIdx.x];
     const int tid = threadIdx.x;
-    const int tiles_x = (J.resolution - 1 + TILE - 1) / TILE;
+    const int tiles_x = P.part_side ? P.part_side : (J.resolution - 1 + TILE - 1) / TILE;
     for (int L = TILE_LEVELS; L < J.n_levels; ++L) {
         const int w = J.level_w[L], ws = J.level_w[L - 1];
         const float* src = J.mip + J.level_off[L - 1];
@@ -257,7 +258,8 @@ static int mip_levels(int R, int64_t* off, int32_t* w) {
 
 extern "C" size_t hc_maxmip_workspace_bytes(int n_jobs, int max_resolution) {
     if (n_jobs <= 0 || max_resolution < 2) return 0;
-    const size_t t = (size_t)(max_resolution - 1 + TILE - 1) / TILE;
+    // ceil(R / 32) blocks per side: the fused frame epilogue's partials (>= k_mip_tiles')
+    const size_t t = (size_t)(max_resolution + TILE - 1) / TILE;
     return (size_t)n_jobs * t * t * 2 * sizeof(float);
 }
 
@@ -305,6 +307,7 @@ int hc::maxmip_launch(const HcMipJob* jobs, int n_jobs, void* workspace, size_t 
     }
     P.tiles_grid = tiles_max;
     P.n_jobs = n_jobs;
+    P.part_side = 0;
     memset(&P.ord, 0, sizeof(P.ord));
     int nc = 0;
     if (ord && ord->n_tiles > 0) {
@@ -319,6 +322,31 @@ int hc::maxmip_launch(const HcMipJob* jobs, int n_jobs, void* workspace, size_t 
     } else {
         dim3 g(tiles_max + order_cols, tiles_max, n_jobs);
         k_mip_tiles<1><<<g, 256, 0, stream>>>(P);
+    }
+    k_mip_top<<<n_jobs + nc, 1024, 0, stream>>>(P);
+    return cuda_status("hc_maxmip");
+}
+
+int hc::maxmip_top_launch(const HcMipJob* jobs, int n_jobs, float* partial, int partial_slots, int part_side,
+                          const OrderJob* ord, cudaStream_t stream) {
+    HC_REQUIRE(jobs && partial, "hc_maxmip: null argument");
+    HC_REQUIRE(n_jobs >= 1 && n_jobs <= 2 * HC_MAX_CASCADES, "hc_maxmip: %d jobs", n_jobs);
+    HC_REQUIRE(part_side >= 1 && part_side * part_side <= partial_slots, "hc_maxmip: partial layout");
+    MipParams P;
+    memset(&P, 0, sizeof(P));
+    for (int k = 0; k < n_jobs; ++k) {
+        HC_REQUIRE(jobs[k].mip && jobs[k].vrange_key && jobs[k].n_levels >= 1 && jobs[k].n_levels <= HC_MAX_LEVELS,
+                   "hc_maxmip: job %d", k);
+        P.j[k] = jobs[k];
+    }
+    P.partial = partial;
+    P.max_tiles = partial_slots;
+    P.n_jobs = n_jobs;
+    P.part_side = part_side;
+    int nc = 0;
+    if (ord && ord->n_tiles > 0) {
+        P.ord = *ord;
+        nc = order_chunks(ord->n_tiles);
     }
     k_mip_top<<<n_jobs + nc, 1024, 0, stream>>>(P);
     return cuda_status("hc_maxmip");

@@ -805,13 +805,35 @@ extern "C" int hc_frame_launch(const HcPlan* plan, const HcCamera* cam, const Hc
         return HC_ECUDA;
     }
     rec(0);
-    int rc = hc_discretize(cr, K, grid, (float)(dom->h_lo - 1.0), buf->counters, stream);
-    if (rc) return rc;
-    rec(1);
-    // the render's tile-queue order is computed inside the two max-mip launches
+    // one launch: rasters + mip levels 0..5 + patch bytes + valid-range partials,
+    // plus the render's tile-queue histograms in extra CTAs
     hc::OrderJob ord{A.tile_cost, A.tile_order, A.tile_counter,
                      A.tile_order ? (int32_t)hc_render_tiles(A.x0, A.y0, A.x1, A.y1) : 0};
-    rc = hc::maxmip_launch(jobs, 2 * K, buf->mip_ws, buf->mip_ws_bytes, &ord, s);
+    hc::DiscMipJob dm;
+    memset(&dm, 0, sizeof(dm));
+    for (int c = 0; c < K; ++c) {
+        dm.mip[c][0] = jobs[2 * c].mip;
+        dm.mip[c][1] = jobs[2 * c + 1].mip;
+        dm.patch_ok[c] = jobs[2 * c].patch_ok;
+    }
+    dm.n_levels = nlev;
+    for (int L = 0; L < 6; ++L) {
+        dm.level_off[L] = L < nlev ? loff[L] : 0;
+        dm.level_w[L] = L < nlev ? lw[L] : 0;
+    }
+    const int side = (R + 31) / 32;
+    dm.partial = (float*)buf->mip_ws;
+    dm.partial_slots = side * side;
+    dm.full = dbg != nullptr;          // debug frames expose the whole pyramid
+    if (!buf->mip_ws || buf->mip_ws_bytes < (size_t)2 * K * dm.partial_slots * 2 * sizeof(float)) {
+        hc::set_error("hc_frame_launch: mip workspace %zu bytes too small", buf->mip_ws_bytes);
+        return HC_ECAPACITY;
+    }
+    int rc = hc::discretize_launch(cr, K, grid, (float)(dom->h_lo - 1.0), buf->counters, &dm, &ord, s);
+    if (rc) return rc;
+    rec(1);
+    // levels >= 6, valid ranges, and the tile-queue scatter in extra CTAs
+    rc = hc::maxmip_top_launch(jobs, 2 * K, dm.partial, dm.partial_slots, side, &ord, s);
     if (rc) return rc;
     rec(2);
     rc = hc::render_launch(&A, A.tile_order != nullptr, s);

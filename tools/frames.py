@@ -1,0 +1,55 @@
+"""Render frames of a benchmark config along its camera path (dev tool, GPU box).
+
+    python tools/frames.py --config C2 --frames 8 [--start 0]
+
+Enqueues `frames` frames (no L2 flush, no read-back), prints the mean per-kernel
+event times and the frame work counters.  Small and quick, so it is the command
+to wrap in ncu:  ncu -k regex:k_discretize -s 3 -c 1 python tools/frames.py ...
+"""
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--frames", type=int, default=8)
+    ap.add_argument("--start", type=int, default=0)
+    a = ap.parse_args()
+    import torch
+    from paper_2201_10887_b200 import _cuda, _engine, build_influence_table
+    from paper_2201_10887_b200.configs import CONFIGS
+    from paper_2201_10887_b200.render import enqueue_frame
+    cfg = CONFIGS[a.config]
+    g = cfg.grid()
+    t = build_influence_table(g, cfg.sigma)
+    st = cfg.settings()
+    mk = lambda: torch.cuda.Event(enable_timing=True)
+    ev = [[mk() for _ in range(4)] for _ in range(a.frames)]
+    for e4 in ev:
+        for e in e4:
+            e.record()
+    torch.cuda.synchronize()
+    cnt = []
+    for i in range(a.frames):
+        buf, plan, _ = enqueue_frame(cfg.path_frame_config(a.start + i), g, t, st, events=_engine.event_handles(ev[i]))
+        cnt.append(buf.counters.clone())
+    torch.cuda.synchronize()
+    mean = lambda xs: sum(xs) / len(xs)
+    names = ("discretize", "mip_top", "render")
+    out = {n: round(mean([e[j].elapsed_time(e[j + 1]) for e in ev]), 4) for j, n in enumerate(names)}
+    c = torch.stack(cnt).double().mean(0).tolist()
+    out["pairs"] = c[_cuda.CNT_PAIRS]
+    out["valid_texels"] = c[_cuda.CNT_VALID]
+    out["node_visits"] = c[_cuda.CNT_NODE_VISITS]
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
