@@ -16,8 +16,11 @@ GPU mask + RBF discretization, max mipmaps, ray casting and shading.
            duration vs MEASURED_PEAKS.json (see DESIGN.md for the unit models).
 `cpu_baseline`: the float64 C oracle port of the reference pipeline
            (oracle/, OpenMP over all host cores) on rank 0, bounded sample.
-N>1: one process per GPU (torchrun), each rank renders its own camera view of
-the same grid (view sharding, no data-path collective): weak scaling; the
+N>1: one process per GPU (torchrun).  C1-C4: each rank renders its own camera
+view of the same grid (view sharding, no data-path collective): weak scaling.
+C5: screen strips of one frame (strong scaling): each rank discretizes its
+strip's footprint, one NCCL MAX all-reduce exchanges the level-5 mips and valid
+partials, each rank traces its strip; e2e gathers the image to rank 0.  The
 reported value is total frames/s, timed as the max over ranks.
 `--impl reference`: times the oracle port of the reference's CPU pipeline on
 the host cores (rank 0 only) for the same config/metric.
@@ -43,7 +46,7 @@ import numpy as np  # noqa: E402
 from paper_2201_10887_b200.configs import PATH_FRAMES  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
-PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "ncu_r2.json")
 B200_SMS = 148
 MUFU_PER_SM_CLK = 16          # ex2 lanes per SM per clock (SURVEY.md §8 d)
 
@@ -351,6 +354,14 @@ def main():
         torch.cuda.synchronize()
 
     def step(i, events=None):
+        if strips and ws > 1:
+            # sharded strip: footprint discretization, the one MAX all-reduce of the
+            # mip exchange buffer (between events 1 and 2), upper mips + the strip's rays
+            f = multi.StripFrame(frame_of(i), g, table, st, rects, rank, events=events)
+            f.stage1()
+            multi.all_reduce_max(f.xchg)
+            f.stage2()
+            return f.buf, f.plan, f.plan_ms
         return enqueue_frame(frame_of(i), g, table, st, rect=rect, events=events)
 
     # ---- warm-up (device-resident path): the last warm-up poses of the path, so the
@@ -421,7 +432,7 @@ def main():
         e2e_ms = [(time.perf_counter() - t0) * 1e3]
     else:
         def e2e_step(i):
-            part = multi.render_strip(frame_of(i), g, table, P, st, rects[rank])
+            part = multi.render_strip(frame_of(i), g, table, P, st, rects[rank], rects=rects, rank=rank)
             img = multi.gather_strips(part, rects, rank, ws) if ws > 1 else part
             if rank == 0:
                 img.cpu()
@@ -451,18 +462,30 @@ def main():
     hbm = float(peaks["hbm_gbs"])
     K = plan.n_active
     R = cfg.resolution
-    _, _, nodes = _engine.mip_shape(R)
-    mip_bytes = 2 * K * (4 * (R * R + nodes) + R * R)
+    off, wl, nodes = _engine.mip_shape(R)
+    # k_mip_top reads level 5 and writes levels >= 6 of 2K pyramids (+ 2K x blocks partials)
+    lv5 = wl[5] * wl[5] if len(wl) > 5 else 0
+    above = nodes - off[6] if len(off) > 6 else 0
+    top_bytes = 2 * K * (4 * (lv5 + above) + 8 * ((R + 31) // 32) ** 2)
+    # HBM bytes the fused discretize writes: rasters (terrain, water f32; valid, mask u8),
+    # mip levels 0..5 of both layers, patch bytes
+    lv05 = off[6] if len(off) > 6 else nodes
+    disc_bytes = K * R * R * 10 + 2 * K * 4 * lv05 + K * (R - 1) ** 2
     trav_bytes = 4 * work["node_visits"] + 20 * work["patch_tests"] + 3 * cfg.width * cfg.height
     mean = lambda xs: sum(xs) / len(xs)
     kernels = {
         "hc_discretize": {"ms": mean(k_disc), "bound": "sfu", "unit": "Gpairs/s",
                           "achieved": work["pairs"] / (mean(k_disc) * 1e-3) / 1e9,
                           "peak": mufu_peak / 1e9, "work_per_launch": work["pairs"],
-                          "work_model": "(valid texel, influence-list entry) pairs; 1 ex2 each"},
-        "hc_maxmip": {"ms": mean(k_mip), "bound": "hbm", "unit": "GB/s",
-                      "achieved": mip_bytes / (mean(k_mip) * 1e-3) / 1e9, "peak": hbm,
-                      "work_per_launch": mip_bytes, "work_model": "2K x (4(R^2+nodes)+R^2) bytes"},
+                          "work_model": "(valid texel, influence-list entry) pairs; 1 ex2 each "
+                                        "(the launch also writes rasters + mip levels 0..5)",
+                          "hbm_bytes_written": disc_bytes,
+                          "hbm_frac": disc_bytes / (mean(k_disc) * 1e-3) / 1e9 / hbm},
+        "hc_mip_top": {"ms": mean(k_mip), "bound": "hbm", "unit": "GB/s",
+                       "achieved": top_bytes / (mean(k_mip) * 1e-3) / 1e9, "peak": hbm,
+                       "work_per_launch": top_bytes,
+                       "work_model": "2K x 4 B x (level-5 nodes + nodes above) + 2K x 8 B x blocks "
+                                     "(a ~10 us launch: latency, not bandwidth)"},
         "hc_render": {"ms": mean(k_ren), "bound": "hbm", "unit": "GB/s",
                       "achieved": trav_bytes / (mean(k_ren) * 1e-3) / 1e9, "peak": hbm,
                       "work_per_launch": trav_bytes,
@@ -471,31 +494,38 @@ def main():
     for k in kernels.values():
         k["frac"] = k["achieved"] / k["peak"]
     l2_gbs = l2_bandwidth_gbs(dev)
-    kernels["hc_maxmip"]["l2_peak_gbs"] = l2_gbs
-    kernels["hc_maxmip"]["frac_l2"] = kernels["hc_maxmip"]["achieved"] / l2_gbs
+    kernels["hc_render"]["l2_peak_gbs"] = l2_gbs
+    kernels["hc_render"]["frac_l2"] = kernels["hc_render"]["achieved"] / l2_gbs
+    kernels["hc_render"]["rays_per_sec"] = 2 * cfg.width * cfg.height / (mean(k_ren) * 1e-3)
     work["pairs_per_valid_texel"] = work["pairs"] / max(work["valid_texels"], 1)
     dominant = max(kernels, key=lambda n: kernels[n]["ms"])
-    traffic = None
+    # what ncu (profiles/ncu_r2.json, `ncu --set full` of this config's frame kernels)
+    # says bounds each kernel: DRAM bytes per launch, issue-active, pipe utilisations
     prof = {}
     try:
         with open(PROFILE_SUMMARY) as fh:
             prof = json.load(fh).get(cfg.name, {})
-        traffic = prof.get(dominant)
     except (OSError, ValueError):
         pass
-    # the issue roofline from the committed ncu capture of this config (fraction of
-    # cycles an instruction issued): where the byte/ex2 roofline is far, this says
-    # whether the kernel is instruction-bound or stalled on latency
     for name, k in kernels.items():
-        ia = prof.get("issue_active", {}).get(name)
-        if ia is not None:
-            k["ncu_issue_active"] = ia
+        if name in prof:
+            k["ncu"] = prof[name]
     d = kernels[dominant]
-    roofline = {"kernel": dominant, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
-                "unit": d["unit"], "frac": d["frac"], "traffic": traffic,
-                "ncu_issue_active": d.get("ncu_issue_active"),
-                "peak_source": f"{peak_kind} MEASURED_PEAKS.json" if d["bound"] == "hbm"
+    nc = d.get("ncu") or {}
+    roofline = {"kernel": dominant, "bound": "hbm" if d["bound"] == "hbm" else "sfu", "achieved": d["achieved"],
+                "peak": d["peak"], "unit": d["unit"], "frac": d["frac"],
+                "traffic": nc.get("dram_bytes"),
+                "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs" if d["bound"] == "hbm"
                 else f"148 SMs x 16 ex2/clk x {sm_max:.0f} MHz ({peak_kind} sm_max_mhz)"}
+    if nc:
+        # the ceiling the kernel actually hits, from the committed ncu capture
+        pipes = {p: nc.get(p) for p in ("fp64_pipe", "xu_pipe", "fma_pipe", "lsu_pipe")}
+        roofline["limiter"] = {"issue_active": nc.get("issue_active"), **pipes,
+                               "occupancy": nc.get("occupancy"), "l1_hit": nc.get("l1_hit"),
+                               "l2_hit": nc.get("l2_hit"), "source": f"profiles/{prof.get('_source')}"}
+        if dominant == "hc_render":
+            roofline["limiter"]["bound"] = "issue/latency (FP64 dependency chains)"
+            roofline["limiter"]["frac_l2"] = d["frac_l2"]
 
     out = None
     if rank == 0:

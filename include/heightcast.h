@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define HC_ABI_VERSION 4
+#define HC_ABI_VERSION 5
 #define HC_MAX_EDGES 32      /* polygon edges per cascade mask          */
 #define HC_MAX_CASCADES 8    /* K (the reference hard-codes 3)           */
 #define HC_MAX_LEVELS 20     /* max-mip levels (R <= 2^19)               */
@@ -370,6 +370,40 @@ typedef struct {
 int hc_frame_launch(const HcPlan *plan, const HcCamera *cam, const HcDomain *dom, const HcGrid *grid,
                     const HcFrameBuffers *buf, const HcShading *shade, const HcRenderDebug *dbg,
                     const int32_t *rect, void *const *events, hc_stream_t stream);
+
+/* ---- screen-strip sharding (C5, SURVEY.md §8 e) ---------------------------
+ *
+ * Every rank plans the same full-view cascades and traces only its pixel strip.
+ * A strip's rays stay inside a 2D ground wedge: apex + a*dir[s][0] + b*dir[s][1]
+ * (a, b >= 0), or anywhere when all[s] != 0.  Stage 1 of a sharded frame
+ * discretizes only the 32x32-texel blocks (level-5 mip nodes) that meet this
+ * rank's wedge dilated by `margin` texels, plus every (rank-th) block that meets
+ * no strip's wedge; it writes each computed block's level-5 nodes and valid-height
+ * partials into `xchg`, -inf for blocks it skipped.  The caller MAX-reduces
+ * `xchg` over the ranks (one NCCL all-reduce of hc_frame_xchg_floats floats),
+ * then stage 2 builds levels >= 6 and the valid ranges from it and renders
+ * `rect`.  Every node a strip ray reads is then the single-GPU value: levels
+ * 0..4 and patches only under blocks the ray's wedge meets, level 5 and above
+ * from the reduction -- strips are bit-identical to the full frame. */
+#define HC_MAX_STRIPS 16
+
+typedef struct {
+    int32_t n_strips, rank;
+    double apex[2];                      /* eye ground point (world) */
+    double dir[HC_MAX_STRIPS][2][2];     /* strip s: wedge boundary directions (world, unit) */
+    int32_t all[HC_MAX_STRIPS];          /* strip s reads the whole plane */
+    double margin;                       /* dilation of a block's square, in texels */
+} HcFootprint;
+
+/* floats of the exchange buffer for K cascades of R^2 (0 if R has < 7 mip levels) */
+size_t hc_frame_xchg_floats(int K, int R);
+/* stage 1 (counters reset, sharded discretize -> xchg) or stage 2 (levels >= 6 +
+ * valid ranges from the reduced xchg, render of rect); events as hc_frame_launch
+ * (stage 1 records 0 and 1, stage 2 records 2 and 3). */
+int hc_frame_stage(int stage, const HcPlan *plan, const HcCamera *cam, const HcDomain *dom, const HcGrid *grid,
+                   const HcFrameBuffers *buf, const HcShading *shade, const HcRenderDebug *dbg,
+                   const int32_t *rect, void *const *events, const HcFootprint *fp, float *xchg,
+                   hc_stream_t stream);
 
 /* Self-test of the hoisted float64 division used by the traversal: counts operand
  * pairs (n pseudo-random + structured) where it differs from IEEE a / b. */

@@ -17,10 +17,11 @@ LIB_DIR = os.path.join(PKG_DIR, "_lib")
 LIB_PATH = os.environ.get("HC_LIB_PATH") or os.path.join(LIB_DIR, "libheightcast_cuda.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 
-HC_ABI_VERSION = 4
+HC_ABI_VERSION = 5
 HC_MAX_EDGES = 32
 HC_MAX_CASCADES = 8
 HC_MAX_LEVELS = 20
+HC_MAX_STRIPS = 16
 HC_OK, HC_EINVAL, HC_ECUDA, HC_ECAPACITY = 0, -1, -2, -3
 (CNT_VISIBLE, CNT_VALID, CNT_ZERO_WEIGHT, CNT_RAYS_HIT, CNT_PAIRS, CNT_NODE_VISITS,
  CNT_PATCH_TESTS) = range(7)
@@ -31,7 +32,8 @@ EXPORTS = ("hc_py_hypot", "hc_visible_hull", "hc_clip_cascades", "hc_fit_layout"
            "hc_abi_version", "hc_last_error", "hc_build_records", "hc_visibility_mask",
            "hc_discretize", "hc_maxmip_workspace_bytes", "hc_maxmip", "hc_render", "hc_render_tiles",
            "hc_render_order_words", "hc_traverse_batch", "hc_eval_points", "hc_influence_workspace_bytes",
-           "hc_influence_build", "hc_frame_launch", "hc_selftest_division", "hc_selftest_patch", "hc_bench_l2_read", "hc_ahf_parse",
+           "hc_influence_build", "hc_frame_launch", "hc_frame_xchg_floats", "hc_frame_stage",
+           "hc_selftest_division", "hc_selftest_patch", "hc_bench_l2_read", "hc_ahf_parse",
            "hc_paint_tiles")
 HC_MAX_HULL = 64
 
@@ -124,6 +126,11 @@ class HcFrameBuffers(C.Structure):
                 ("capacity", _i32), ("resolution", _i32), ("width", _i32), ("height", _i32)]
 
 
+class HcFootprint(C.Structure):
+    _fields_ = [("n_strips", _i32), ("rank", _i32), ("apex", _d * 2), ("dir", ((_d * 2) * 2) * HC_MAX_STRIPS),
+                ("all", _i32 * HC_MAX_STRIPS), ("margin", _d)]
+
+
 class HcAhfInfo(C.Structure):
     _fields_ = [("xmin", _d), ("ymin", _d), ("xmax", _d), ("ymax", _d), ("min_cell", _d),
                 ("count", _i64), ("error_line", _i64), ("non_ascii", _i32), ("reserved", _i32)]
@@ -196,6 +203,11 @@ def lib():
     L.hc_frame_launch.argtypes = [C.POINTER(HcPlan), C.POINTER(HcCamera), C.POINTER(HcDomain), C.POINTER(HcGrid),
                                   C.POINTER(HcFrameBuffers), C.POINTER(HcShading), C.POINTER(HcRenderDebug),
                                   _vp, _vp, _vp]
+    L.hc_frame_xchg_floats.restype = C.c_size_t
+    L.hc_frame_xchg_floats.argtypes = [C.c_int, C.c_int]
+    L.hc_frame_stage.argtypes = [C.c_int, C.POINTER(HcPlan), C.POINTER(HcCamera), C.POINTER(HcDomain),
+                                 C.POINTER(HcGrid), C.POINTER(HcFrameBuffers), C.POINTER(HcShading),
+                                 C.POINTER(HcRenderDebug), _vp, _vp, C.POINTER(HcFootprint), _vp, _vp]
     L.hc_influence_workspace_bytes.restype = C.c_size_t
     L.hc_influence_workspace_bytes.argtypes = [C.c_int]
     L.hc_influence_build.argtypes = [C.POINTER(HcGrid), C.POINTER(HcInfluenceBins), C.c_double, _vp, _vp,

@@ -173,13 +173,18 @@ def event_handles(events):
 
 
 def launch_planned(buf: FrameBuffers, plan, camera_native, domain_native, ginf, shade, rect=None, stream=None,
-                   events=None):
+                   events=None, stage=None, footprint=None, xchg=None):
     """Enqueue one planned frame on `stream` (no host sync).  `events`: optional
-    event_handles() array recorded instead of the buffers' own events."""
+    event_handles() array recorded instead of the buffers' own events.  With
+    `stage` (1 or 2), `footprint` (HcFootprint) and `xchg` (float32 device tensor of
+    hc_frame_xchg_floats): one stage of a sharded screen-strip frame."""
     r = None if rect is None else (C.c_int32 * 4)(*rect)
-    _cuda.check(_cuda.lib().hc_frame_launch(
-        C.byref(plan), C.byref(camera_native), C.byref(domain_native), C.byref(ginf.view), C.byref(buf.native),
-        C.byref(shade), C.byref(buf.dbg_native) if buf.dbg_native is not None else None,
-        C.cast(r, C.c_void_p) if r is not None else None,
-        C.cast(buf.ev_handles if events is None else events, C.c_void_p),
-        _cuda.stream_ptr(stream)), "hc_frame_launch")
+    args = (C.byref(plan), C.byref(camera_native), C.byref(domain_native), C.byref(ginf.view), C.byref(buf.native),
+            C.byref(shade), C.byref(buf.dbg_native) if buf.dbg_native is not None else None,
+            C.cast(r, C.c_void_p) if r is not None else None,
+            C.cast(buf.ev_handles if events is None else events, C.c_void_p))
+    if stage is None:
+        _cuda.check(_cuda.lib().hc_frame_launch(*args, _cuda.stream_ptr(stream)), "hc_frame_launch")
+    else:
+        _cuda.check(_cuda.lib().hc_frame_stage(stage, *args, C.byref(footprint), _cuda.ptr(xchg),
+                                               _cuda.stream_ptr(stream)), "hc_frame_stage")

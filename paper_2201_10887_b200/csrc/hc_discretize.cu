@@ -139,8 +139,13 @@ struct DiscParams {
     int64_t level_off[TILE_LEVELS];
     int32_t level_w[TILE_LEVELS];
     float* partial;                 // [2K][max_tiles][2] valid min/max per block
-    int32_t full_mips;              // 0: blocks outside the mask write only their top node (see below)
+    int32_t full_mips;              // 0: blocks outside the mask skip mip level 0 (see below)
     OrderJob ord;                   // tile-queue order histogram of the frame's k_render (n_tiles 0: none)
+    // screen-strip sharding (heightcast.h HcFootprint): xchg != NULL selects blocks by
+    // footprint and writes level-5 nodes + partials (-min, max) there instead
+    float* xchg;                    // [2K][l5_nodes] level-5 nodes, then [2K][max_tiles][2] partials
+    int32_t l5_nodes;               // level_w[5]^2
+    HcFootprint fp;
 };
 
 // Pair-interleaved anchored records in quads (see heightcast.h HcGrid): one warp per
@@ -225,6 +230,43 @@ __global__ void __launch_bounds__(256) k_visibility_mask(HcCascadeRaster c) {
     const double px = dadd(c.origin_x, dmul((double)ix, c.texel));
     const double py = dadd(c.origin_y, dmul((double)iy, c.texel));
     c.mask[(int64_t)iy * c.resolution + ix] = texel_visible(c, px, py) ? 1 : 0;
+}
+
+// Does the square [x0, x1] x [y0, y1] meet the wedge apex + a d0 + b d1 (a, b >= 0,
+// angle(d0, d1) < pi)?  Separating axes of a convex polygon pair: the wedge's two edge
+// normals and the square's axes.  Callers dilate the square by a few texels, far more
+// than the rounding of these float64 expressions or of the rays' positions.
+__device__ __forceinline__ bool square_meets_wedge(double x0, double y0, double x1, double y1, const double* A,
+                                                   const double (*D)[2]) {
+    const double cx[4] = {x0, x1, x0, x1}, cy[4] = {y0, y0, y1, y1};
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        double nx = -D[e][1], ny = D[e][0];
+        if (nx * D[1 - e][0] + ny * D[1 - e][1] > 0.0) nx = -nx, ny = -ny;    // outward
+        bool outside = true;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) outside = outside && (nx * (cx[c] - A[0]) + ny * (cy[c] - A[1]) > 0.0);
+        if (outside) return false;
+    }
+    const double xlo = (D[0][0] < 0.0 || D[1][0] < 0.0) ? -INFINITY : A[0];
+    const double xhi = (D[0][0] > 0.0 || D[1][0] > 0.0) ? INFINITY : A[0];
+    const double ylo = (D[0][1] < 0.0 || D[1][1] < 0.0) ? -INFINITY : A[1];
+    const double yhi = (D[0][1] > 0.0 || D[1][1] > 0.0) ? INFINITY : A[1];
+    return !(x1 < xlo || x0 > xhi || y1 < ylo || y0 > yhi);
+}
+
+// Sharded frames: does this rank discretize block (bx, by) of cascade c?  Its own
+// strip's wedge meets the block's node square (dilated), or no strip's wedge does
+// and the block is this rank's by round robin.
+__device__ bool block_selected(const HcFootprint& fp, const HcCascadeRaster& c, int bx, int by, int blk_id) {
+    const double m = fp.margin;
+    const double x0 = c.origin_x + ((double)bx - m) * c.texel, x1 = c.origin_x + ((double)bx + 32.0 + m) * c.texel;
+    const double y0 = c.origin_y + ((double)by - m) * c.texel, y1 = c.origin_y + ((double)by + 32.0 + m) * c.texel;
+    auto meets = [&](int s) { return fp.all[s] != 0 || square_meets_wedge(x0, y0, x1, y1, fp.apex, fp.dir[s]); };
+    if (meets(fp.rank)) return true;
+    for (int s = 0; s < fp.n_strips; ++s)
+        if (s != fp.rank && meets(s)) return false;
+    return blk_id % fp.n_strips == fp.rank;
 }
 
 // Classify a box of texels [x0, x1] x [y0, y1] against the mask polygon without
@@ -365,6 +407,13 @@ __device__ __forceinline__ Unit plan_unit(int u, int lane, const int* s_cell, co
     return U;
 }
 
+// valid min/max partial of block rb of (cascade kc, layer): the frame workspace, or
+// the exchange buffer of a sharded frame
+__device__ __forceinline__ float* partial_slot(const DiscParams& P, int kc, int layer, int rb) {
+    const int64_t slot = ((int64_t)(2 * kc + layer) * P.max_tiles + rb) * 2;
+    return P.xchg ? P.xchg + (int64_t)2 * P.n_cascades * P.l5_nodes + slot : P.partial + slot;
+}
+
 template <bool MIPS>
 __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_constant__ DiscParams P,
                                                        const __grid_constant__ HcGrid g) {
@@ -388,6 +437,19 @@ __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_
     const int R = c.resolution, n0 = R - 1;
     const int bx = (rb % bs) * BLK, by = (rb / bs) * BLK;
     if (bx >= R || by >= R) return;
+    if (MIPS && P.xchg && !block_selected(P.fp, c, bx, by, kc * bs * bs + rb)) {
+        // not this rank's: the MAX-reduction's identity for its level-5 node and partials
+        if (threadIdx.x < 2) {
+            const int wl5 = P.level_w[5];
+            if ((bx >> 5) < wl5 && (by >> 5) < wl5)
+                P.xchg[(int64_t)(2 * kc + threadIdx.x) * P.l5_nodes + (by >> 5) * wl5 + (bx >> 5)] = -INFINITY;
+            float* pp = P.xchg + (int64_t)2 * P.n_cascades * P.l5_nodes +
+                        ((int64_t)(2 * kc + threadIdx.x) * P.max_tiles + rb) * 2;
+            pp[0] = -INFINITY;
+            pp[1] = -INFINITY;
+        }
+        return;
+    }
 
     extern __shared__ __align__(16) unsigned char smem[];
     int* s_cell = reinterpret_cast<int*>(smem);                                    // [NT]
@@ -439,13 +501,22 @@ __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_
             }
         }
         if (MIPS) {
-            // The block's top node (level 5, or the pyramid top for small rasters) is the
-            // sentinel, below every ray height of the traversal slab [hmin, hmax]
-            // (hmin >= h_lo - float rounding > sentinel = h_lo - 1), so the traversal
-            // steps over it and never reads the block's lower levels or patch bytes
-            // (_kernels.py:134-166).  They are written only when the caller inspects the
-            // whole pyramid (debug frames).
-            const int L0 = P.full_mips ? 0 : min(TILE_LEVELS, P.n_levels) - 1;
+            // Every node is the sentinel, below every ray height of the traversal slab
+            // [hmin, hmax] (hmin >= h_lo - float rounding > sentinel = h_lo - 1).  A ray
+            // entering the block from above skips its top node, but a level-0 walk that
+            // steps across the block's edge ascends one level at a time
+            // (_kernels.py:194-213) and visits its level-1..4 nodes and, below them,
+            // patch bytes: those are written every frame, so nothing the render reads
+            // is left over from an earlier frame.  Level 0 itself is not read by
+            // k_render (it recomputes level-0 maxima from the corners); it is written
+            // when the caller inspects the whole pyramid (debug frames).
+            if (!P.full_mips && P.patch_ok[kc]) {
+                for (int e = tid; e < BLK * BLK; e += 256) {
+                    const int gx = bx + (e & 31), gy = by + (e >> 5);
+                    if (gx < n0 && gy < n0) P.patch_ok[kc][(int64_t)gy * n0 + gx] = 0;
+                }
+            }
+            const int L0 = P.full_mips ? 0 : 1;
             for (int L = L0; L < TILE_LEVELS && L < P.n_levels; ++L) {
                 const int side = BLK >> L, wl = P.level_w[L];
                 for (int e = tid; e < side * side; e += 256) {
@@ -455,12 +526,16 @@ __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_
                         P.mip[kc][0][o] = sentinel;
                         P.mip[kc][1][o] = sentinel;
                         if (L == 0 && P.patch_ok[kc]) P.patch_ok[kc][(int64_t)gy * n0 + gx] = 0;
+                        if (L == 5 && P.xchg) {
+                            P.xchg[(int64_t)(2 * kc) * P.l5_nodes + (int64_t)gy * wl + gx] = sentinel;
+                            P.xchg[(int64_t)(2 * kc + 1) * P.l5_nodes + (int64_t)gy * wl + gx] = sentinel;
+                        }
                     }
                 }
             }
             if (tid < 2) {
-                float* pp = P.partial + ((int64_t)(2 * kc + tid) * P.max_tiles + rb) * 2;
-                pp[0] = INFINITY;
+                float* pp = partial_slot(P, kc, tid, rb);
+                pp[0] = P.xchg ? -INFINITY : INFINITY;     // xchg holds -min
                 pp[1] = -INFINITY;
             }
         }
@@ -754,6 +829,10 @@ __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_
                 const int64_t o = P.level_off[L] + (int64_t)gy * wl + gx;
                 P.mip[kc][0][o] = m0;
                 P.mip[kc][1][o] = m1;
+                if (L == 5 && P.xchg) {
+                    P.xchg[(int64_t)(2 * kc) * P.l5_nodes + (int64_t)gy * wl + gx] = m0;
+                    P.xchg[(int64_t)(2 * kc + 1) * P.l5_nodes + (int64_t)gy * wl + gx] = m1;
+                }
             }
         }
         __syncthreads();
@@ -777,8 +856,8 @@ __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_
             a = fminf(a, s_red[tid][0][w]);
             b = fmaxf(b, s_red[tid][1][w]);
         }
-        float* pp = P.partial + ((int64_t)(2 * kc + tid) * P.max_tiles + rb) * 2;
-        pp[0] = a;
+        float* pp = partial_slot(P, kc, tid, rb);
+        pp[0] = P.xchg ? -a : a;
         pp[1] = b;
     }
 }
@@ -914,6 +993,15 @@ int hc::discretize_launch(const HcCascadeRaster* cascades, int n_cascades, const
         }
         P.partial = mips->partial;
         P.full_mips = mips->full;
+        if (mips->xchg) {
+            HC_REQUIRE(mips->fp && mips->n_levels >= 7, "hc_frame_stage: sharding needs a footprint and R >= 66");
+            HC_REQUIRE(mips->fp->n_strips >= 1 && mips->fp->n_strips <= HC_MAX_STRIPS && mips->fp->rank >= 0 &&
+                           mips->fp->rank < mips->fp->n_strips,
+                       "hc_frame_stage: bad footprint (%d strips, rank %d)", mips->fp->n_strips, mips->fp->rank);
+            P.xchg = mips->xchg;
+            P.l5_nodes = mips->level_w[5] * mips->level_w[5];
+            P.fp = *mips->fp;
+        }
         if (ord && ord->n_tiles > 0) {
             HC_REQUIRE(ord->cost && ord->order && ord->counter, "hc_discretize: order job with null pointers");
             P.ord = *ord;

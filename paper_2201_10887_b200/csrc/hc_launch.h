@@ -32,6 +32,8 @@ struct DiscMipJob {
     float* partial;                          // [2K][partial_slots][2]
     int32_t partial_slots;                   // >= ceil(R / 32)^2
     int32_t full;                            // write every level under blocks outside the mask
+    float* xchg;                             // sharded frame: exchange buffer (heightcast.h HcFootprint), or NULL
+    const HcFootprint* fp;                   // with xchg: the strips' ground wedges
 };
 
 int discretize_launch(const HcCascadeRaster* cascades, int n_cascades, const HcGrid* grid, float sentinel,
@@ -39,7 +41,7 @@ int discretize_launch(const HcCascadeRaster* cascades, int n_cascades, const HcG
 // levels >= 6 of each job from level 5, and the job's valid range from `partial`
 // ([n_jobs][partial_slots][2], part_side^2 used); extra CTAs scatter the tile order
 int maxmip_top_launch(const HcMipJob* jobs, int n_jobs, float* partial, int partial_slots, int part_side,
-                      const OrderJob* ord, cudaStream_t stream);
+                      const OrderJob* ord, cudaStream_t stream, const float* xchg = nullptr);
 int maxmip_launch(const HcMipJob* jobs, int n_jobs, void* workspace, size_t workspace_bytes, const OrderJob* ord,
                   cudaStream_t stream);
 // order_ready: the tile order (and queue head) were produced by maxmip_launch

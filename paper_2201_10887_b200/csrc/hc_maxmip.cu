@@ -40,6 +40,8 @@ struct MipParams {
     int32_t n_jobs;                 // k_mip_top: CTAs past n_jobs scatter the order
     int32_t part_side;              // k_mip_top: partials per side (0: (R - 1 + 31) / 32, k_mip_tiles')
     OrderJob ord;                   // tile-queue order of the frame's k_render (n_tiles 0: none)
+    const float* xchg;              // k_mip_top of a sharded frame: reduced level-5 nodes + partials
+    int32_t l5_nodes;
 };
 
 __device__ __forceinline__ int ceil_shift(int n, int s) { return (n + (1 << s) - 1) >> s; }
@@ -193,6 +195,13 @@ __global__ void __launch_bounds__(1024) k_mip_top(const __grid_constant__ MipPar
     const HcMipJob& J = P.j[blockIdx.x];
     const int tid = threadIdx.x;
     const int tiles_x = P.part_side ? P.part_side : (J.resolution - 1 + TILE - 1) / TILE;
+    if (P.xchg) {
+        // sharded frame: level 5 from the ranks' MAX-reduced exchange buffer
+        const int w5 = J.level_w[TILE_LEVELS - 1];
+        const float* src = P.xchg + (int64_t)blockIdx.x * w5 * w5;
+        for (int e = tid; e < w5 * w5; e += blockDim.x) J.mip[J.level_off[TILE_LEVELS - 1] + e] = src[e];
+        __syncthreads();
+    }
     for (int L = TILE_LEVELS; L < J.n_levels; ++L) {
         const int w = J.level_w[L], ws = J.level_w[L - 1];
         const float* src = J.mip + J.level_off[L - 1];
@@ -212,9 +221,11 @@ __global__ void __launch_bounds__(1024) k_mip_top(const __grid_constant__ MipPar
     // fold the per-CTA partials (min/max are order independent)
     __shared__ float red[2][32];
     float vmin = INFINITY, vmax = -INFINITY;
-    const float* pp = P.partial + (int64_t)blockIdx.x * P.max_tiles * 2;
+    const float* pp = (P.xchg ? P.xchg + (int64_t)P.n_jobs * P.l5_nodes : P.partial) +
+                      (int64_t)blockIdx.x * P.max_tiles * 2;
+    const float sgn = P.xchg ? -1.0f : 1.0f;       // the exchange buffer holds -min
     for (int e = tid; e < tiles_x * tiles_x; e += blockDim.x) {
-        vmin = fminf(vmin, pp[2 * e]);
+        vmin = fminf(vmin, sgn * pp[2 * e]);
         vmax = fmaxf(vmax, pp[2 * e + 1]);
     }
     for (int s = 16; s > 0; s >>= 1) {
@@ -275,6 +286,7 @@ int hc::maxmip_launch(const HcMipJob* jobs, int n_jobs, void* workspace, size_t 
                2 * HC_MAX_CASCADES);
     if (n_jobs == 0) return HC_OK;
     MipParams P;
+    memset(&P, 0, sizeof(P));
     int tiles_max = 0, rmax = 0;
     for (int k = 0; k < n_jobs; ++k) {
         const HcMipJob& J = jobs[k];
@@ -328,7 +340,7 @@ int hc::maxmip_launch(const HcMipJob* jobs, int n_jobs, void* workspace, size_t 
 }
 
 int hc::maxmip_top_launch(const HcMipJob* jobs, int n_jobs, float* partial, int partial_slots, int part_side,
-                          const OrderJob* ord, cudaStream_t stream) {
+                          const OrderJob* ord, cudaStream_t stream, const float* xchg) {
     HC_REQUIRE(jobs && partial, "hc_maxmip: null argument");
     HC_REQUIRE(n_jobs >= 1 && n_jobs <= 2 * HC_MAX_CASCADES, "hc_maxmip: %d jobs", n_jobs);
     HC_REQUIRE(part_side >= 1 && part_side * part_side <= partial_slots, "hc_maxmip: partial layout");
@@ -343,6 +355,11 @@ int hc::maxmip_top_launch(const HcMipJob* jobs, int n_jobs, float* partial, int 
     P.max_tiles = partial_slots;
     P.n_jobs = n_jobs;
     P.part_side = part_side;
+    if (xchg) {
+        HC_REQUIRE(jobs[0].n_levels >= 7, "hc_maxmip: sharded frames need >= 7 levels");
+        P.xchg = xchg;
+        P.l5_nodes = jobs[0].level_w[TILE_LEVELS - 1] * jobs[0].level_w[TILE_LEVELS - 1];
+    }
     int nc = 0;
     if (ord && ord->n_tiles > 0) {
         P.ord = *ord;

@@ -678,9 +678,11 @@ void level_shape(int R, int64_t* off, int32_t* w, int* n) {
 
 }  // namespace
 
-extern "C" int hc_frame_launch(const HcPlan* plan, const HcCamera* cam, const HcDomain* dom, const HcGrid* grid,
-                               const HcFrameBuffers* buf, const HcShading* shade, const HcRenderDebug* dbg,
-                               const int32_t* rect, void* const* events, hc_stream_t stream) {
+// stages: bit 0 = counters + discretize (+ mips 0..5), bit 1 = mips >= 6 + render
+static int frame_launch(int stages, const HcPlan* plan, const HcCamera* cam, const HcDomain* dom, const HcGrid* grid,
+                        const HcFrameBuffers* buf, const HcShading* shade, const HcRenderDebug* dbg,
+                        const int32_t* rect, void* const* events, const HcFootprint* fp, float* xchg,
+                        hc_stream_t stream) {
     if (!plan || !cam || !dom || !grid || !buf || !shade) {
         hc::set_error("hc_frame_launch: null argument");
         return HC_EINVAL;
@@ -800,11 +802,11 @@ extern "C" int hc_frame_launch(const HcPlan* plan, const HcCamera* cam, const Hc
     A.tile_order = full ? buf->tile_order : nullptr;
     if (dbg) A.dbg = *dbg;
 
-    if (buf->counters && cudaMemsetAsync(buf->counters, 0, sizeof(uint64_t) * HC_COUNTERS, s) != cudaSuccess) {
+    if ((stages & 1) && buf->counters &&
+        cudaMemsetAsync(buf->counters, 0, sizeof(uint64_t) * HC_COUNTERS, s) != cudaSuccess) {
         hc::set_error("hc_frame_launch: counter reset failed");
         return HC_ECUDA;
     }
-    rec(0);
     // one launch: rasters + mip levels 0..5 + patch bytes + valid-range partials,
     // plus the render's tile-queue histograms in extra CTAs
     hc::OrderJob ord{A.tile_cost, A.tile_order, A.tile_counter,
@@ -829,15 +831,54 @@ extern "C" int hc_frame_launch(const HcPlan* plan, const HcCamera* cam, const Hc
         hc::set_error("hc_frame_launch: mip workspace %zu bytes too small", buf->mip_ws_bytes);
         return HC_ECAPACITY;
     }
-    int rc = hc::discretize_launch(cr, K, grid, (float)(dom->h_lo - 1.0), buf->counters, &dm, &ord, s);
-    if (rc) return rc;
-    rec(1);
-    // levels >= 6, valid ranges, and the tile-queue scatter in extra CTAs
-    rc = hc::maxmip_top_launch(jobs, 2 * K, dm.partial, dm.partial_slots, side, &ord, s);
-    if (rc) return rc;
-    rec(2);
-    rc = hc::render_launch(&A, A.tile_order != nullptr, s);
-    if (rc) return rc;
-    rec(3);
+    dm.xchg = xchg;
+    dm.fp = fp;
+    if (xchg && (!fp || nlev < 7)) {
+        hc::set_error("hc_frame_stage: sharded frames need a footprint and R >= 66 (got R = %d)", R);
+        return HC_EINVAL;
+    }
+    if (stages & 1) {
+        rec(0);
+        int rc = hc::discretize_launch(cr, K, grid, (float)(dom->h_lo - 1.0), buf->counters, &dm, &ord, s);
+        if (rc) return rc;
+        rec(1);
+    }
+    if (stages & 2) {
+        // levels >= 6, valid ranges, and the tile-queue scatter in extra CTAs
+        int rc = hc::maxmip_top_launch(jobs, 2 * K, dm.partial, dm.partial_slots, side, &ord, s, xchg);
+        if (rc) return rc;
+        rec(2);
+        rc = hc::render_launch(&A, A.tile_order != nullptr, s);
+        if (rc) return rc;
+        rec(3);
+    }
     return HC_OK;
+}
+
+extern "C" int hc_frame_launch(const HcPlan* plan, const HcCamera* cam, const HcDomain* dom, const HcGrid* grid,
+                               const HcFrameBuffers* buf, const HcShading* shade, const HcRenderDebug* dbg,
+                               const int32_t* rect, void* const* events, hc_stream_t stream) {
+    return frame_launch(3, plan, cam, dom, grid, buf, shade, dbg, rect, events, nullptr, nullptr, stream);
+}
+
+extern "C" size_t hc_frame_xchg_floats(int K, int R) {
+    int64_t loff[HC_MAX_LEVELS];
+    int32_t lw[HC_MAX_LEVELS];
+    int nlev = 0;
+    if (K < 1 || K > HC_MAX_CASCADES || R < 2) return 0;
+    level_shape(R, loff, lw, &nlev);
+    if (nlev < 7) return 0;
+    const size_t side = (size_t)(R + 31) / 32;
+    return 2 * (size_t)K * ((size_t)lw[5] * lw[5] + 2 * side * side);
+}
+
+extern "C" int hc_frame_stage(int stage, const HcPlan* plan, const HcCamera* cam, const HcDomain* dom,
+                              const HcGrid* grid, const HcFrameBuffers* buf, const HcShading* shade,
+                              const HcRenderDebug* dbg, const int32_t* rect, void* const* events,
+                              const HcFootprint* fp, float* xchg, hc_stream_t stream) {
+    if ((stage != 1 && stage != 2) || !xchg || !fp) {
+        hc::set_error("hc_frame_stage: stage %d (1 or 2) with footprint and exchange buffer", stage);
+        return HC_EINVAL;
+    }
+    return frame_launch(stage, plan, cam, dom, grid, buf, shade, dbg, rect, events, fp, xchg, stream);
 }

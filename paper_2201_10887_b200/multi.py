@@ -1,23 +1,23 @@
 """Multi-GPU partitioning of the frame path (SURVEY.md §8 e), one process per GPU.
 
-Two decompositions, both without a data-path collective:
-
 * camera batches (C4): views are independent; rank r renders views
   r, r+N, r+2N, ... of a batch against the grid resident in its own HBM.
-  `shard_views` assigns them; throughput scales weakly.
+  `shard_views` assigns them; no data-path collective, weak scaling.
 * screen strips (C5): every rank plans the SAME full-view cascades (the host
-  planner is deterministic) and discretizes the full cascades, so its rasters,
-  pyramids and valid ranges equal the single-GPU ones bit for bit -- the
-  traversal's slab clip needs the global valid range (render.py:127,144), which
-  this gets without any all-reduce -- then traces only its vertical strip of
-  pixels (`HcRenderArgs.x0..x1`).  Strip widths can be rebalanced from per-strip
-  costs (`balance_strips`).  The only collective is the optional image gather to
-  rank 0 at the end of the frame (`gather_strips`, NCCL over NVLink on GPUs,
-  gloo in the CPU tests).
-
-Pixels of a strip are identical to the same pixels of a full frame
-(tests/test_gpu_parity.py::test_screen_strips_equal_full_frame), so sharded
-frames are bit-identical to single-GPU frames at any GPU count.
+  planner is deterministic) and traces only its vertical strip of pixels
+  (`HcRenderArgs.x0..x1`).  Each rank builds its own cascades: it discretizes
+  only the 32x32-texel blocks its strip's rays can reach -- the blocks that meet
+  the strip's ground wedge (`strip_footprint`), dilated by 2.5 texels -- plus a
+  round-robin share of the blocks no strip reaches.  The traversal's slab clip
+  needs the global valid range (render.py:127,144, _kernels.py:105-115) and its
+  upper mip levels need every block, so stage 1 of the frame writes each block's
+  level-5 max-mip nodes and valid-height partials to an exchange buffer and ONE
+  NCCL all-reduce (MAX, ~0.3 MB at C5) combines the ranks' buffers; stage 2
+  builds mip levels >= 6 and the valid ranges from it and traces the strip.
+  Every node and texel a strip ray reads then holds its single-GPU value, so
+  strips are bit-identical to the full frame (heightcast.h HcFootprint).  The
+  image is gathered to rank 0 (`gather_strips`, NCCL over NVLink; gloo on CPU).
+  Strip widths can be rebalanced from per-tile costs (`balance_strips`).
 """
 
 from __future__ import annotations
@@ -71,16 +71,17 @@ def balance_strips(tile_cost, width: int, height: int, world: int, tile_w: int =
 def gather_strips(strip: "torch.Tensor", rects, rank: int, world: int, group=None, dst: int = 0):
     """Assemble per-rank (H, x1-x0, 3) uint8 strips into one (H, W, 3) image on `dst`.
 
-    Uses all_gather on equally padded strips (works with NCCL device tensors and
-    gloo host tensors); returns the image on `dst`, None elsewhere."""
+    A gather to `dst` only (the other ranks send their strip once) of equally padded
+    strips; works with NCCL device tensors and gloo host tensors.  Returns the image
+    on `dst`, None elsewhere."""
     import torch
     import torch.distributed as dist
     H = strip.shape[0]
     wmax = max(x1 - x0 for x0, x1 in rects)
     padded = torch.zeros((H, wmax, 3), dtype=strip.dtype, device=strip.device)
     padded[:, :strip.shape[1]] = strip
-    parts = [torch.empty_like(padded) for _ in range(world)]
-    dist.all_gather(parts, padded, group=group)
+    parts = [torch.empty_like(padded) for _ in range(world)] if rank == dst else None
+    dist.gather(padded, parts, dst=dst, group=group)
     if rank != dst:
         return None
     W = rects[-1][1]
@@ -90,16 +91,179 @@ def gather_strips(strip: "torch.Tensor", rects, rank: int, world: int, group=Non
     return out
 
 
-def render_strip(config, grid, table, params, settings, rect):
+FOOTPRINT_MARGIN = 2.5        # texels of dilation of a block's square (SURVEY.md §8 e)
+_WIDEN = 1e-9                  # radians: each wedge boundary turned outward
+
+
+def strip_wedges(camera, width: int, height: int, rects):
+    """Ground wedges of screen strips: for strip [x0, x1) the 2D directions of all its
+    pixel rays (render.py:100-110: d = look + xs right + ys up, any ys of the image)
+    lie between two boundary directions.  Returns [(all_plane, d0, d1)] per strip:
+    the image of the strip's (xs, ys) rectangle under d -> d_xy is a parallelogram
+    whose cone from the origin is spanned by its corners; if the corners do not fit
+    in an open half-plane (the view looks nearly straight down, or the strip spans
+    >= 180 degrees) the strip may reach the whole plane."""
+    import math
+    right, up, look = camera.basis()
+    th = math.tan(math.radians(camera.fov_y) / 2.0)
+    ys = ((1.0 - (0.5 / height) * 2.0) * th, (1.0 - ((height - 0.5) / height) * 2.0) * th)
+    out = []
+    for x0, x1 in rects:
+        if x1 <= x0:
+            out.append((True, (1.0, 0.0), (0.0, 1.0)))
+            continue
+        xs = ((((x0 + 0.5) / width) * 2.0 - 1.0) * th * camera.aspect,
+              (((x1 - 0.5) / width) * 2.0 - 1.0) * th * camera.aspect)
+        c = [np.asarray(look, dtype=np.float64) + x * right + y * up for x in xs for y in ys]
+        c2 = np.array([v[:2] for v in c])
+        scale = max(float(np.linalg.norm(v)) for v in c)
+        n2 = np.linalg.norm(c2, axis=1)
+        if np.any(n2 <= 1e-6 * scale):
+            out.append((True, (1.0, 0.0), (0.0, 1.0)))
+            continue
+        base = c2[0] / n2[0]
+        ang = [math.atan2(base[0] * v[1] - base[1] * v[0], base[0] * v[0] + base[1] * v[1]) for v in c2]
+        lo, hi = min(ang) - _WIDEN, max(ang) + _WIDEN
+        if hi - lo >= math.pi - 1e-6:
+            out.append((True, (1.0, 0.0), (0.0, 1.0)))
+            continue
+        rot = lambda a: (base[0] * math.cos(a) - base[1] * math.sin(a), base[0] * math.sin(a) + base[1] * math.cos(a))
+        out.append((False, rot(lo), rot(hi)))
+    return out
+
+
+def strip_footprint(camera, width: int, height: int, rects, rank: int, margin: float = FOOTPRINT_MARGIN):
+    """HcFootprint of `rank` among the strips `rects` (the C struct of heightcast.h)."""
+    from . import _cuda
+    if not 0 <= rank < len(rects) or len(rects) > _cuda.HC_MAX_STRIPS:
+        raise ValueError(f"rank {rank} of {len(rects)} strips (max {_cuda.HC_MAX_STRIPS})")
+    fp = _cuda.HcFootprint()
+    fp.n_strips, fp.rank, fp.margin = len(rects), rank, float(margin)
+    fp.apex[0], fp.apex[1] = float(camera.eye[0]), float(camera.eye[1])
+    for s, (whole, d0, d1) in enumerate(strip_wedges(camera, width, height, rects)):
+        fp.all[s] = 1 if whole else 0
+        fp.dir[s][0][0], fp.dir[s][0][1] = d0
+        fp.dir[s][1][0], fp.dir[s][1][1] = d1
+    return fp
+
+
+def square_meets_wedge(x0, y0, x1, y1, apex, d0, d1) -> bool:
+    """Host twin of the kernel's block test (hc_discretize.cu square_meets_wedge)."""
+    D = (d0, d1)
+    cs = ((x0, y0), (x1, y0), (x0, y1), (x1, y1))
+    for e in range(2):
+        nx, ny = -D[e][1], D[e][0]
+        if nx * D[1 - e][0] + ny * D[1 - e][1] > 0.0:
+            nx, ny = -nx, -ny
+        if all(nx * (cx - apex[0]) + ny * (cy - apex[1]) > 0.0 for cx, cy in cs):
+            return False
+    inf = float("inf")
+    xlo = -inf if (d0[0] < 0 or d1[0] < 0) else apex[0]
+    xhi = inf if (d0[0] > 0 or d1[0] > 0) else apex[0]
+    ylo = -inf if (d0[1] < 0 or d1[1] < 0) else apex[1]
+    yhi = inf if (d0[1] > 0 or d1[1] > 0) else apex[1]
+    return not (x1 < xlo or x0 > xhi or y1 < ylo or y0 > yhi)
+
+
+def exchange_floats(settings) -> int:
+    from . import _cuda
+    return int(_cuda.lib().hc_frame_xchg_floats(settings.count, settings.resolution))
+
+
+def all_reduce_max(xchg, group=None):
+    """The sharded frame's one collective: elementwise MAX of the ranks' exchange buffers."""
+    import torch.distributed as dist
+    dist.all_reduce(xchg, op=dist.ReduceOp.MAX, group=group)
+
+
+class StripFrame:
+    """One rank's screen strip of a frame, in two stages around the exchange
+    (heightcast.h hc_frame_stage).  `stage1()` plans and enqueues the footprint
+    discretization; the caller MAX-reduces `xchg` across ranks; `stage2()` enqueues
+    the upper mips, valid ranges and the strip's rays.  Pixels land in the frame
+    buffers' `rgb[:, x0:x1]`."""
+
+    def __init__(self, config, grid, table, settings, rects, rank, slot=0, debug=False, events=None):
+        import torch
+        from .render import prepare_frame
+        self.rects, self.rank = rects, rank
+        self.rect = (rects[rank][0], 0, rects[rank][1], config.height)
+        self.events = events
+        self.prep = prepare_frame(config, grid, table, settings, debug, slot)
+        self.visible = self.prep is not None
+        self.world = len(rects)
+        if not self.visible:
+            return
+        self.buf, self.plan, self.plan_ms, self._launch = self.prep
+        n = exchange_floats(settings)
+        if self.world > 1 and n == 0:
+            raise ValueError("screen-strip sharding needs cascades of at least 66 texels")
+        xb = getattr(self.buf, "_xchg", None)
+        if xb is None or xb.numel() != n:
+            xb = self.buf._xchg = torch.empty(max(n, 1), dtype=torch.float32, device=self.buf.rgb.device)
+        self.xchg = xb
+        self.footprint = strip_footprint(config.camera, config.width, config.height, rects, rank)
+
+    def stage1(self):
+        if self.world == 1:          # a whole frame: no exchange
+            self._launch(rect=self.rect, events=self.events)
+        else:
+            self._launch(rect=self.rect, events=self.events, stage=1, footprint=self.footprint, xchg=self.xchg)
+
+    def stage2(self):
+        if self.world > 1:
+            self._launch(rect=self.rect, events=self.events, stage=2, footprint=self.footprint, xchg=self.xchg)
+
+    def strip(self):
+        x0, _, x1, _ = self.rect
+        return self.buf.rgb[:, x0:x1]
+
+
+def render_strip(config, grid, table, params, settings, rect, rects=None, rank=None, reduce=all_reduce_max):
     """Render pixel columns rect=(x0, x1) of the full frame on this rank's GPU.
 
-    Returns the (H, x1-x0, 3) uint8 device tensor (a copy), or None if nothing is visible."""
-    from .render import enqueue_frame
-    x0, x1 = rect
+    With `rects` (every rank's strip) and `rank`, the frame is sharded: this rank
+    discretizes only its strip's footprint and `reduce(xchg)` (default: NCCL/gloo
+    all-reduce MAX over the default group) combines the ranks' mip exchange
+    buffers.  Without them the rank computes the full cascades (no collective).
+    Returns the (H, x1-x0, 3) uint8 device tensor (a copy), or None if nothing is
+    visible (the same on every rank: the plan is deterministic)."""
     if table.sigma != params.sigma:
         raise ValueError("influence table was built for a different sigma")
-    queued = enqueue_frame(config, grid, table, settings, rect=(x0, 0, x1, config.height))
-    if queued is None:
+    if rects is None:
+        rects, rank = [tuple(rect)], 0
+    elif tuple(rects[rank]) != tuple(rect):
+        raise ValueError("rect is not rects[rank]")
+    f = StripFrame(config, grid, table, settings, rects, rank)
+    if not f.visible:
         return None
-    buf = queued[0]
-    return buf.rgb[:, x0:x1].clone()
+    f.stage1()
+    if f.world > 1:
+        reduce(f.xchg)
+    f.stage2()
+    return f.strip().clone()
+
+
+def render_strips_one_gpu(config, grid, table, params, settings, world: int, rects=None):
+    """All `world` ranks of a sharded frame emulated on this GPU one after the other
+    (stage 1 of every rank, the MAX reduction as torch.maximum, stage 2 of every
+    rank): the (H, W, 3) image assembled from the strips, and each rank's frame
+    counters (HC_CNT_*: its texels, pairs, rays).  For parity tests; nothing waits on another rank."""
+    import torch
+    rects = rects or screen_strips(config.width, world)
+    frames = [StripFrame(config, grid, table, settings, rects, r, slot=r) for r in range(world)]
+    if not frames[0].visible:
+        return None, None
+    for f in frames:
+        f.stage1()
+    if world > 1:
+        red = frames[0].xchg.clone()
+        for f in frames[1:]:
+            torch.maximum(red, f.xchg, out=red)
+        for f in frames:
+            f.xchg.copy_(red)
+    for f in frames:
+        f.stage2()
+    img = torch.cat([f.strip() for f in frames], dim=1).cpu().numpy()
+    counters = [f.buf.counters.cpu().numpy().copy() for f in frames]
+    return img, counters

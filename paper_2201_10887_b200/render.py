@@ -179,6 +179,19 @@ def enqueue_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable
     Returns (buffers, plan, plan_ms) without waiting for the GPU, or None when
     nothing is visible.  The device-resident half of `render_frame`; pixels stay
     in `buffers.rgb` until read back."""
+    prep = prepare_frame(config, grid, table, settings, debug, slot)
+    if prep is None:
+        return None
+    buf, plan, plan_ms, launch = prep
+    launch(rect=rect, events=events)
+    return buf, plan, plan_ms
+
+
+def prepare_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable,
+                  settings: CascadeSettings = CascadeSettings(), debug: bool = False, slot: int = 0):
+    """Plan one frame on the host and bind its buffer set: (buffers, plan, plan_ms,
+    launch) or None when nothing is visible; `launch(**kw)` enqueues the frame (or
+    one stage of a sharded frame, see multi.py) via _engine.launch_planned."""
     tp = time.perf_counter()
     plan = plan_native(config.camera, grid, settings.resolution, settings.overlap, settings.count)
     if plan.status != 0:
@@ -191,9 +204,13 @@ def enqueue_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable
     dom = getattr(grid, "_hc_domain", None)
     if dom is None:
         dom = grid._hc_domain = _cascade_domain(grid)
-    _engine.launch_planned(buf, plan, config.camera.native(), dom, ginf, _shading(config), rect=rect,
-                           events=events)
-    return buf, plan, plan_ms
+    cam = config.camera.native()
+    shade = _shading(config)
+
+    def launch(**kw):
+        _engine.launch_planned(buf, plan, cam, dom, ginf, shade, **kw)
+
+    return buf, plan, plan_ms, launch
 
 
 def render_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable, params: RbfParams,

@@ -124,3 +124,45 @@ def rbf_points(domain, seed: int, n: int):
     x = np.clip(x, domain.xmin + 1e-6, domain.xmax - 1e-6)
     y = np.clip(y, domain.ymin + 1e-6, domain.ymax - 1e-6)
     return np.stack([x, y], axis=1)
+
+
+# ---- scalar twins (traverse_cascade / cast_through_cascades, raycast.py:195-256)
+
+TWIN_GRID = {"kind": "pond", "seed": 42, "cells": 3000}
+TWIN_POSES = [
+    {"eye": (150.0, 120.0, 160.0), "look_at": (1100.0, 1150.0, 20.0), "fov_y": 55.0, "res": 128},
+    {"eye": (1900.0, 300.0, 90.0), "look_at": (900.0, 1300.0, 10.0), "fov_y": 70.0, "res": 256},
+    {"eye": (1024.0, -150.0, 300.0), "look_at": (1024.0, 1024.0, 0.0), "fov_y": 40.0, "res": 64},
+]
+TWIN_W, TWIN_H = 48, 32          # image whose every pixel's ray is cast
+
+
+def twin_camera_args(pose):
+    eye, la = pose["eye"], pose["look_at"]
+    return dict(eye=eye, look_dir=tuple(b - a for a, b in zip(eye, la)), up=(0.0, 0.0, 1.0),
+                fov_y=pose["fov_y"], aspect=TWIN_W / TWIN_H, near_clip=1.0, far_clip=6000.0)
+
+
+def twin_raster(origin, texel, R, mask):
+    """Deterministic float32-representable (terrain, water, valid) for a cascade layout.
+
+    A smooth polynomial of the texel centre plus integer-hash noise, built from
+    + and * only (no libm), so every host computes the same bits.  Water lies
+    above the terrain inside a disc, equals it elsewhere."""
+    i = np.arange(R, dtype=np.float64)
+    x = origin[0] + i * texel
+    y = origin[1] + i * texel
+    X, Y = np.meshgrid(x, y)
+    u, v = (X - 1024.0) / 1024.0, (Y - 1024.0) / 1024.0
+    h = 25.0 + 18.0 * u * v - 9.0 * u * u * u + 6.0 * v * v
+    iy, ix = np.meshgrid(np.arange(R, dtype=np.int64), np.arange(R, dtype=np.int64), indexing="ij")
+    kx = np.floor(X / 7.0).astype(np.int64)
+    ky = np.floor(Y / 7.0).astype(np.int64)
+    hsh = ((kx * 73856093) ^ (ky * 19349663)) % 1009
+    h = h + hsh.astype(np.float64) * (4.0 / 1009.0)
+    terrain = h.astype(np.float32).astype(np.float64)
+    pond = (X - 1000.0) ** 2 + (Y - 1100.0) ** 2 < 350.0 ** 2
+    water = np.where(pond, np.maximum(terrain, 31.25), terrain).astype(np.float32).astype(np.float64)
+    valid = np.ascontiguousarray(mask, dtype=bool).copy()
+    valid[(ix * 7 + iy * 3) % 97 == 0] = False          # scattered invalid texels
+    return np.ascontiguousarray(terrain), np.ascontiguousarray(water), valid

@@ -47,11 +47,24 @@ def _worker(rank, world, port, q):
     x0, x1 = rects[rank]
     strip = torch.from_numpy(full[:, x0:x1].copy())
     out = multi.gather_strips(strip, rects, rank, world)
+    # the sharded frame's exchange: each rank's computed entries, -inf elsewhere; the
+    # MAX all-reduce must leave every rank with every entry
+    rng = np.random.default_rng(5)
+    truth = rng.normal(size=4096).astype(np.float32)
+    truth[::7] = -np.float32(rng.normal(size=truth[::7].size)) ** 2   # negated minima
+    owner = rng.integers(0, world, truth.size)
+    extra = rng.random(truth.size) < 0.3                    # blocks computed by two ranks
+    mine = (owner == rank) | (extra & (owner == (rank + 1) % world))
+    xchg = torch.from_numpy(np.where(mine, truth, -np.inf).astype(np.float32))
+    multi.all_reduce_max(xchg)
+    xchg_ok = bool(np.array_equal(xchg.numpy(), truth))
     # weak-scaling timing reduction used by bench.py: max over ranks
     t = torch.tensor([float(rank + 1)])
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
-        q.put((bool(np.array_equal(out.numpy(), full)), float(t.item())))
+        q.put((bool(np.array_equal(out.numpy(), full)) and xchg_ok, float(t.item())))
+    else:
+        assert out is None and xchg_ok
     dist.barrier()
     dist.destroy_process_group()
 
@@ -68,3 +81,74 @@ def test_gather_strips_gloo(world):
     for p in procs:
         p.join(timeout=60)
     assert ok and tmax == float(world)
+
+
+def _block_selected(fp_args, s, x0, y0, x1, y1, blk_id):
+    """Host twin of hc_discretize.cu block_selected for strip s."""
+    apex, wedges = fp_args
+    meets = lambda r: wedges[r][0] or multi.square_meets_wedge(x0, y0, x1, y1, apex, wedges[r][1], wedges[r][2])
+    if meets(s):
+        return True
+    if any(meets(r) for r in range(len(wedges)) if r != s):
+        return False
+    return blk_id % len(wedges) == s
+
+
+def _cameras():
+    from paper_2201_10887_b200.cascade import CameraView
+    from paper_2201_10887_b200.configs import CONFIGS
+    cams = [CONFIGS[n].path_camera(i) for n in ("C2", "C5") for i in (0, 30, 60)]
+    rng = np.random.default_rng(11)
+    for _ in range(6):
+        eye = (float(rng.uniform(-300, 2300)), float(rng.uniform(-300, 2300)), float(rng.uniform(20, 900)))
+        tgt = (float(rng.uniform(200, 1800)), float(rng.uniform(200, 1800)), 0.0)
+        cams.append(CameraView(eye=eye, look_dir=tuple(b - a for a, b in zip(eye, tgt)), up=(0.0, 0.0, 1.0),
+                               fov_y=float(rng.uniform(30, 100)), aspect=16 / 9, near_clip=1.0, far_clip=6000.0))
+    # straight down: every strip may reach the whole plane
+    cams.append(CameraView(eye=(1000.0, 1000.0, 500.0), look_dir=(1e-9, 0.0, -1.0), up=(0.0, 1.0, 0.0),
+                           fov_y=60.0, aspect=16 / 9, near_clip=1.0, far_clip=6000.0))
+    return cams
+
+
+def test_strip_wedges_contain_every_ray_and_blocks_are_covered():
+    """Every pixel ray of a strip stays inside its wedge (sampled along the ray on the
+    ground), so the blocks it crosses are selected by its rank; and every block of a
+    cascade is selected by at least one rank (block_selected's host twin)."""
+    from paper_2201_10887_b200.render import camera_ray_dirs
+    W, H = 384, 216
+    for cam in _cameras():
+        dirs = camera_ray_dirs(cam, W, H)
+        for world in (2, 3, 8):
+            rects = multi.screen_strips(W, world)
+            wedges = multi.strip_wedges(cam, W, H, rects)
+            apex = (float(cam.eye[0]), float(cam.eye[1]))
+            for s, ((x0, x1), (whole, d0, d1)) in enumerate(zip(rects, wedges)):
+                if whole:
+                    continue
+                d = dirs[::9, x0:x1:3].reshape(-1, 3)
+                for tt in (1.0, 37.0, 400.0, 5000.0):
+                    px = apex[0] + tt * d[:, 0]
+                    py = apex[1] + tt * d[:, 1]
+                    # a point on the ray: a degenerate square must meet the wedge
+                    for x, y in zip(px[::17], py[::17]):
+                        assert multi.square_meets_wedge(x - 1e-6, y - 1e-6, x + 1e-6, y + 1e-6, apex, d0, d1)
+            # coverage of a synthetic 512^2 cascade (16 x 16 blocks of 32 texels, 2 m texels)
+            org, tex = (apex[0] - 400.0, apex[1] - 300.0), 2.0
+            fp = (apex, wedges)
+            for by in range(16):
+                for bx in range(16):
+                    sq = (org[0] + (32 * bx - 2.5) * tex, org[1] + (32 * by - 2.5) * tex,
+                          org[0] + (32 * bx + 34.5) * tex, org[1] + (32 * by + 34.5) * tex)
+                    assert any(_block_selected(fp, r, *sq, by * 16 + bx) for r in range(world))
+
+
+def test_strip_wedge_of_full_width_view_is_the_view():
+    """One strip = the whole image: the wedge is the horizontal field of view."""
+    import math
+    from paper_2201_10887_b200.cascade import CameraView
+    cam = CameraView(eye=(0.0, 0.0, 100.0), look_dir=(1.0, 0.0, -0.2), up=(0.0, 0.0, 1.0), fov_y=60.0,
+                     aspect=2.0, near_clip=1.0, far_clip=6000.0)
+    (whole, d0, d1), = multi.strip_wedges(cam, 1000, 500, [(0, 1000)])
+    assert not whole
+    a0, a1 = math.atan2(d0[1], d0[0]), math.atan2(d1[1], d1[0])
+    assert a0 < 0 < a1 and abs(a0 + a1) < 1e-6

@@ -5,7 +5,7 @@
 
 Writes profiles/<tag>.md (key metrics per kernel) and merges per-launch DRAM
 traffic (dram__bytes_read.sum + dram__bytes_write.sum) into
-profiles/ncu_traffic.json, which bench.py reports as roofline.traffic.
+profiles/ncu_r2.json, which bench.py reports as roofline.traffic / limiter.
 """
 
 import argparse
@@ -47,7 +47,7 @@ METRICS = [
 ]
 
 KERNEL_KEY = {"k_render": "hc_render", "k_discretize": "hc_discretize", "k_mip_tiles": "hc_maxmip",
-              "k_mip_top": "hc_maxmip"}
+              "k_mip_top": "hc_mip_top"}
 
 
 def raw_rows(rep):
@@ -85,34 +85,41 @@ def summarise(rep, tag, config):
         lines.append(f"| {label} (`{m}`) | " + " | ".join(vals) + " |")
     with open(os.path.join(PROF, f"{tag}.md"), "w") as fh:
         fh.write("\n".join(lines) + "\n")
-    # traffic per launch (bytes), summed for kernels that make up one ABI call
-    path = os.path.join(PROF, "ncu_traffic.json")
+    # per-kernel metrics for bench.py (profiles/ncu_r2.json): DRAM traffic per launch and
+    # the pipe / issue / occupancy figures that say what bounds each kernel
+    path = os.path.join(PROF, "ncu_r2.json")
     data = json.load(open(path)) if os.path.exists(path) else {}
-    per = defaultdict(float)
-    issue = defaultdict(lambda: [0.0, 0.0])     # key -> [sum(duration * issue active), sum(duration)]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    pct = {"issue_active": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+           "fp64_pipe": "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+           "fma_pipe": "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+           "xu_pipe": "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+           "lsu_pipe": "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+           "occupancy": "sm__warps_active.avg.pct_of_peak_sustained_active",
+           "l1_hit": "l1tex__t_sector_hit_rate.pct", "l2_hit": "lts__t_sector_hit_rate.pct"}
+    cfg = {"_source": os.path.basename(rep)}
+    seen = set()
     for short, r in kernels:
         key = KERNEL_KEY.get(short.replace("void ", "").split("<")[0].strip())
-        if key is None:
+        if key is None or key in seen:          # first launch of each kernel
             continue
-        dur = to_float(r[col["gpu__time_duration.sum"]]) or 0.0
-        ia = to_float(r[col["smsp__issue_active.avg.pct_of_peak_sustained_active"]])
-        if ia is not None:
-            issue[key][0] += dur * ia / 100.0
-            issue[key][1] += dur
-        rd = to_float(r[col["dram__bytes_read.sum"]])
-        wr = to_float(r[col["dram__bytes_write.sum"]])
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-        rd *= scale[units[col["dram__bytes_read.sum"]]]
-        wr *= scale[units[col["dram__bytes_write.sum"]]]
-        per[key] += rd + wr
-    data.setdefault(config, {}).update({k: v for k, v in per.items()})
-    data[config]["_source"] = os.path.basename(rep)
-    # fraction of cycles the SM sub-partitions issued an instruction (duration-weighted
-    # over the kernels of one ABI call): the issue roofline of latency-bound kernels
-    data[config]["issue_active"] = {k: round(a / d, 4) for k, (a, d) in issue.items() if d > 0}
+        seen.add(key)
+        get = lambda m: to_float(r[col[m]]) if m in col else None
+        rd = get("dram__bytes_read.sum") * scale[units[col["dram__bytes_read.sum"]]]
+        wr = get("dram__bytes_write.sum") * scale[units[col["dram__bytes_write.sum"]]]
+        dur = get("gpu__time_duration.sum")
+        dur_us = dur * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(units[col["gpu__time_duration.sum"]], 1.0)
+        k = {"dram_bytes": rd + wr, "duration_us": round(dur_us, 2),
+             "registers": get("launch__registers_per_thread")}
+        for name, m in pct.items():
+            v = get(m)
+            k[name] = None if v is None else round(v / 100.0, 4)
+        k["stall_long_scoreboard"] = get("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio")
+        cfg[key] = k
+    data[config] = cfg
     with open(path, "w") as fh:
         json.dump(data, fh, indent=1, sort_keys=True)
-    print("wrote", os.path.join(PROF, f"{tag}.md"), dict(per))
+    print("wrote", os.path.join(PROF, f"{tag}.md"), {k: v["dram_bytes"] for k, v in cfg.items() if k[0] != "_"})
 
 
 def launches(csv_path, tag):
