@@ -244,6 +244,14 @@ int hc_ahf_parse(const char *text, int64_t len, HcAhfInfo *info, double *cells, 
 int hc_paint_tiles(const int64_t *x0, const int64_t *y0, const int64_t *span, int64_t n, int64_t ntx,
                    int64_t nty, int stop_on_overlap, int32_t *index, int64_t *clash);
 
+/* The same tile index painted in HBM (grid.py:154-177 for a grid whose squares do
+ * not overlap): x0, y0, span are device int64 [n]; index device int32 [nty][ntx];
+ * *painted (device uint64) receives the number of painted tiles.  It equals the
+ * summed clipped cell areas iff no two squares overlap; otherwise the caller
+ * replays hc_paint_tiles on the host for the reference's first-clash semantics. */
+int hc_paint_tiles_device(const int64_t *x0, const int64_t *y0, const int64_t *span, int64_t n, int64_t ntx,
+                          int64_t nty, int32_t *index, uint64_t *painted, hc_stream_t stream);
+
 /* ---- entry points ------------------------------------------------------ */
 
 int hc_abi_version(void);

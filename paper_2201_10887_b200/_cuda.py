@@ -34,7 +34,7 @@ EXPORTS = ("hc_py_hypot", "hc_visible_hull", "hc_clip_cascades", "hc_fit_layout"
            "hc_render_order_words", "hc_traverse_batch", "hc_eval_points", "hc_influence_workspace_bytes",
            "hc_influence_build", "hc_frame_launch", "hc_frame_xchg_floats", "hc_frame_stage",
            "hc_selftest_division", "hc_selftest_patch", "hc_bench_l2_read", "hc_ahf_parse",
-           "hc_paint_tiles")
+           "hc_paint_tiles", "hc_paint_tiles_device")
 HC_MAX_HULL = 64
 
 _vp = C.c_void_p
@@ -222,6 +222,7 @@ def lib():
     L.hc_eval_points.argtypes = [C.POINTER(HcGrid), _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
     L.hc_ahf_parse.argtypes = [C.c_char_p, _i64, C.POINTER(HcAhfInfo), _vp, _i64]
     L.hc_paint_tiles.argtypes = [_vp, _vp, _vp, _i64, _i64, _i64, C.c_int, _vp, _vp]
+    L.hc_paint_tiles_device.argtypes = [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _vp, _vp]
     ver = L.hc_abi_version()
     if ver != HC_ABI_VERSION:
         raise HeightcastCudaError(f"libheightcast_cuda ABI {ver}, expected {HC_ABI_VERSION}")

@@ -148,7 +148,9 @@ class GridDevice:
         self.size = f64(grid.sizes)
         self.terrain = f64(grid.terrain)
         self.depth = f64(grid.water_depth)
-        self.tile_index = torch.from_numpy(np.array(grid.tile_index, copy=True)).to(device)
+        painted = grid.device_tile_index(device)        # painted in this GPU's HBM: no upload
+        self.tile_index = painted if painted is not None else \
+            torch.from_numpy(np.array(grid.tile_index, copy=True)).to(device)
         self._influence = {}
 
     def influence(self, table) -> InfluenceDevice:
@@ -164,7 +166,7 @@ class GridDevice:
         g.cx, g.cy, g.size = self.cx.data_ptr(), self.cy.data_ptr(), self.size.data_ptr()
         g.terrain, g.depth = self.terrain.data_ptr(), self.depth.data_ptr()
         g.tile_index = self.tile_index.data_ptr()
-        nty, ntx = self.grid.tile_index.shape
+        nty, ntx = self.tile_index.shape
         g.ntx, g.nty = ntx, nty
         d = self.grid.domain
         g.xmin, g.ymin, g.min_cell = d.xmin, d.ymin, self.grid.min_cell_size

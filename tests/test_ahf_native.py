@@ -103,3 +103,39 @@ def test_native_tile_painter_reports_overlaps_like_numpy():
         b, cb = g._paint_numpy(stop)
         assert ca == cb == (0, 1)
         assert np.array_equal(a, b)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,seed,cells,max_depth", [("pond", 7, 100_000, 7), ("pond", 11, 300_000, 9),
+                                                       ("hill", 3, 5000, None), ("ramp", 0, 4096, None)])
+def test_gpu_tile_painter_matches_host(cuda, kind, seed, cells, max_depth):
+    """hc_paint_tiles_device (the index painted in HBM) equals the host
+    painter's index (itself pinned to the reference's tile_index digests) tile for tile;
+    the frame kernels read the painted tensor without an upload."""
+    import torch
+    from paper_2201_10887_b200 import synth
+    g = synth.generate_synthetic(kind, seed, cells, max_depth=max_depth)
+    dev_index = g.device_tile_index(cuda)
+    assert dev_index is not None, "grid was not painted on the GPU"
+    host = synth.generate_synthetic(kind, seed, cells, max_depth=max_depth, native_paint=False).tile_index
+    assert torch.equal(dev_index, torch.from_numpy(np.ascontiguousarray(host)).to(cuda))
+    assert np.array_equal(g.tile_index, host)                   # the lazy host download
+    assert g.device_view(cuda).tile_index.data_ptr() == dev_index.data_ptr()
+
+
+@pytest.mark.gpu
+def test_gpu_tile_painter_detects_overlaps(cuda):
+    """Overlapping squares: the painted-tile count falls short of the summed areas and
+    the reference's sequential paint names the first clash (same message as the host)."""
+    from paper_2201_10887_b200 import AdaptiveGrid, GridFormatError, Rect
+    centers = np.array([[1.0, 1.0], [3.0, 3.0], [2.0, 2.0], [7.0, 7.0]])
+    sizes = np.array([2.0, 2.0, 4.0, 2.0])
+    z = np.zeros(4)
+    h = AdaptiveGrid(Rect(0, 0, 8, 8), 2.0, centers, sizes, z + 10, z, check_overlap=False, native_paint=False)
+    first = h._paint_numpy(True)[1]
+    assert first == (0, 2)
+    with pytest.raises(GridFormatError, match="cells 0 and 2 overlap"):
+        AdaptiveGrid(Rect(0, 0, 8, 8), 2.0, centers, sizes, z + 10, z)
+    g = AdaptiveGrid(Rect(0, 0, 8, 8), 2.0, centers, sizes, z + 10, z, check_overlap=False)
+    assert g.device_tile_index(cuda) is None                    # overlap: the host index is kept
+    assert np.array_equal(g.tile_index, h.tile_index) and g.find_overlap() == first

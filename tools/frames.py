@@ -21,6 +21,9 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--frames", type=int, default=8)
     ap.add_argument("--start", type=int, default=0)
+    ap.add_argument("--strips", default="",
+                    help="emulate N sharded screen-strip ranks on this GPU: per-rank stage-1 "
+                         "(footprint discretization) and stage-2 (mips + strip render) event times")
     a = ap.parse_args()
     import torch
     from paper_2201_10887_b200 import _cuda, _engine, build_influence_table
@@ -31,6 +34,39 @@ def main():
     t = build_influence_table(g, cfg.sigma)
     st = cfg.settings()
     mk = lambda: torch.cuda.Event(enable_timing=True)
+    for n_strips in [int(x) for x in a.strips.split(",") if x]:
+        from paper_2201_10887_b200 import multi
+        rects = multi.screen_strips(cfg.width, n_strips)
+        rows = []
+        for i in range(a.frames):
+            fc = cfg.path_frame_config(a.start + i)
+            evs = [[mk() for _ in range(4)] for _ in rects]
+            for e4 in evs:
+                for e in e4:
+                    e.record()
+            fr = [multi.StripFrame(fc, g, t, st, rects, r, slot=r, events=_engine.event_handles(evs[r]))
+                  for r in range(n_strips)]
+            for f in fr:
+                f.stage1()
+            torch.cuda.synchronize()
+            red = fr[0].xchg.clone()
+            for f in fr[1:]:
+                torch.maximum(red, f.xchg, out=red)
+            for f in fr:
+                f.xchg.copy_(red)
+            for f in fr:
+                f.stage2()
+            torch.cuda.synchronize()
+            rows.append([(e[0].elapsed_time(e[1]), e[2].elapsed_time(e[3]),
+                          int(f.buf.counters[_cuda.CNT_PAIRS])) for e, f in zip(evs, fr)])
+        mean = lambda xs: sum(xs) / len(xs)
+        out = {"strips": n_strips, "rects": rects,
+               "discretize_ms": [round(mean([r[k][0] for r in rows]), 4) for k in range(n_strips)],
+               "render_ms": [round(mean([r[k][1] for r in rows]), 4) for k in range(n_strips)],
+               "pairs": [mean([r[k][2] for r in rows]) for k in range(n_strips)]}
+        print(json.dumps(out), flush=True)
+    if a.strips:
+        return
     ev = [[mk() for _ in range(4)] for _ in range(a.frames)]
     for e4 in ev:
         for e in e4:
