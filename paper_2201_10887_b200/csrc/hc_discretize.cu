@@ -54,17 +54,19 @@ namespace hc {
 constexpr double NEG_HALF_LOG2E = -0.72134752044448170368;
 // r2 >= 12.25 (3.5 sigma, rbf.py:29-32) <=> q = r2 * NEG_HALF_LOG2E <= Q_CUT
 constexpr float Q_CUT = (float)(12.25 * NEG_HALF_LOG2E);
-#ifndef DISC_BATCH
-#define DISC_BATCH 4               // record pairs per batch of the per-lane path
-#endif
 #ifndef DISC_STAGE_PAIRS
-#define DISC_STAGE_PAIRS 128       // 2 CTAs per SM (76: 3 CTAs per SM, measured slower)
+#define DISC_STAGE_PAIRS 96        // 2 CTAs per SM, ~85 KB shared memory each (the rest of the 256 KB
+                                   // stays L1 for the lookups and gathers); measured 32-128 / 2-3 CTAs
+                                   // per SM: 96 best
 #endif
 #ifndef DISC_MIN_CTAS
 #define DISC_MIN_CTAS 2
 #endif
 constexpr int STAGE_PAIRS = DISC_STAGE_PAIRS;   // record pairs per warp buffer, shared by up to STAGE_GROUPS cells
-constexpr int STAGE_GROUPS = 8;
+#ifndef DISC_STAGE_GROUPS
+#define DISC_STAGE_GROUPS 12       // cells per staged unit (8 / 12 / 16 measured: 12 best)
+#endif
+constexpr int STAGE_GROUPS = DISC_STAGE_GROUPS;
 constexpr int DISC_WARPS = 8;
 constexpr int BLK = 32;            // texels per block side (= level-5 mip node)
 constexpr int TILE_LEVELS = 6;     // mip levels 0..5 reduced per block
