@@ -507,9 +507,25 @@ def main():
             prof = json.load(fh).get(cfg.name, {})
     except (OSError, ValueError):
         pass
+    clk_hz = None
     for name, k in kernels.items():
         if name in prof:
             k["ncu"] = prof[name]
+    # issue roofline: warp instructions per unit of work from the ncu capture (per pair
+    # for k_discretize, per node visit for k_render), times this run's work per launch,
+    # over the live launch time, against 4 warp-instructions/clk/SM at the run's clock
+    pw = prof.get("_work", {})
+    unit_of = {"hc_discretize": "pairs", "hc_render": "node_visits"}
+    for name, k in kernels.items():
+        wi = (k.get("ncu") or {}).get("warp_instructions")
+        u = unit_of.get(name)
+        if wi and u and pw.get(u) and work.get(u):
+            clk_hz = clk_hz or 1e6 * float(clocks.summary().get("sm_mhz") or sm_max)
+            inst = wi / pw[u] * work[u]
+            peak_i = B200_SMS * 4 * clk_hz
+            k["issue_roofline"] = {"warp_instructions_per_launch": inst, "achieved_per_s": inst / (k["ms"] * 1e-3),
+                                   "peak_per_s": peak_i, "frac": inst / (k["ms"] * 1e-3) / peak_i,
+                                   "model": f"ncu warp instructions per {u} x this run's {u}"}
     d = kernels[dominant]
     nc = d.get("ncu") or {}
     roofline = {"kernel": dominant, "bound": "hbm" if d["bound"] == "hbm" else "sfu", "achieved": d["achieved"],
@@ -526,6 +542,8 @@ def main():
         if dominant == "hc_render":
             roofline["limiter"]["bound"] = "issue/latency (FP64 dependency chains)"
             roofline["limiter"]["frac_l2"] = d["frac_l2"]
+        if d.get("issue_roofline"):
+            roofline["limiter"]["issue_frac"] = d["issue_roofline"]["frac"]
 
     out = None
     if rank == 0:

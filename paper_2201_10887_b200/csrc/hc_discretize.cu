@@ -63,6 +63,9 @@ constexpr float Q_CUT = (float)(12.25 * NEG_HALF_LOG2E);
 #define DISC_MIN_CTAS 2
 #endif
 constexpr int STAGE_PAIRS = DISC_STAGE_PAIRS;   // record pairs per warp buffer, shared by up to STAGE_GROUPS cells
+#ifndef DISC_GATHER_PREFETCH
+#define DISC_GATHER_PREFETCH 1     // gathered units: 0 none, 1 per-lane line prefetches, 2 bulk prefetch
+#endif
 #ifndef DISC_STAGE_GROUPS
 #define DISC_STAGE_GROUPS 12       // cells per staged unit (8 / 12 / 16 measured: 12 best)
 #endif
@@ -124,6 +127,15 @@ __device__ __forceinline__ void prefetch_l2(const void* p, int bytes) {
     const uintptr_t a1 = ((uintptr_t)p + (uintptr_t)bytes + 15) & ~(uintptr_t)15;
     if (a1 > a0)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+}
+
+// the same from every lane at once: one prefetch.global.L2 per 128-byte line (a
+// bulk prefetch takes uniform operands, so per-lane ranges would be issued one
+// lane at a time)
+__device__ __forceinline__ void prefetch_lines_l2(const void* p, int bytes) {
+    const uintptr_t a0 = (uintptr_t)p & ~(uintptr_t)127;
+    const uintptr_t a1 = (uintptr_t)p + (uintptr_t)bytes;
+    for (uintptr_t a = a0; a < a1; a += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
 }
 
 struct DiscParams {
@@ -519,7 +531,10 @@ __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_
                 }
             }
             const int L0 = P.full_mips ? 0 : 1;
-            for (int L = L0; L < TILE_LEVELS && L < P.n_levels; ++L) {
+#pragma unroll
+            for (int L = 0; L < TILE_LEVELS; ++L) {      // unrolled: side is a constant
+                if (L < L0) continue;
+                if (L >= P.n_levels) break;
                 const int side = BLK >> L, wl = P.level_w[L];
                 for (int e = tid; e < side * side; e += 256) {
                     const int gx = (bx >> L) + e % side, gy = (by >> L) + e / side;
@@ -688,7 +703,11 @@ __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_
                 // lanes walk different lists: stream each whole list into L2 at once so
                 // the loads below wait for L2 rather than DRAM
                 const float4* q = grec + (int64_t)U.pb * QUAD;
+#if DISC_GATHER_PREFETCH == 1
+                prefetch_lines_l2(q, U.np * 16 * QUAD);
+#elif DISC_GATHER_PREFETCH == 2
                 prefetch_l2(q, U.np * 16 * QUAD);
+#endif
                 for (int v = 0; v < U.np; ++v) quad4_global(A, nrx, nry, nrem, q + v * QUAD);
             }
         }
@@ -806,7 +825,9 @@ __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_
     }
     __syncthreads();
     // levels 1..5 in place: after level L, lv[.][y][x] for y, x < BLK >> L holds level L
-    for (int L = 1; L < TILE_LEVELS && L < P.n_levels; ++L) {
+#pragma unroll
+    for (int L = 1; L < TILE_LEVELS; ++L) {              // unrolled: side is a constant
+        if (L >= P.n_levels) break;
         const int side = BLK >> L;
         const int wl = P.level_w[L];
         float m0 = 0.f, m1 = 0.f;

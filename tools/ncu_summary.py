@@ -63,7 +63,7 @@ def to_float(s):
         return None
 
 
-def summarise(rep, tag, config):
+def summarise(rep, tag, config, work=None):
     head, units, rows = raw_rows(rep)
     col = {c: i for i, c in enumerate(head)}
     lines = [f"# ncu --set full summary: {tag}", "", f"source: `{os.path.basename(rep)}` "
@@ -108,14 +108,20 @@ def summarise(rep, tag, config):
         rd = get("dram__bytes_read.sum") * scale[units[col["dram__bytes_read.sum"]]]
         wr = get("dram__bytes_write.sum") * scale[units[col["dram__bytes_write.sum"]]]
         dur = get("gpu__time_duration.sum")
-        dur_us = dur * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(units[col["gpu__time_duration.sum"]], 1.0)
+        dur_us = dur * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(
+            units[col["gpu__time_duration.sum"]], 1.0)
         k = {"dram_bytes": rd + wr, "duration_us": round(dur_us, 2),
-             "registers": get("launch__registers_per_thread")}
+             "registers": get("launch__registers_per_thread"),
+             "warp_instructions": get("smsp__inst_executed.sum")}
         for name, m in pct.items():
             v = get(m)
             k[name] = None if v is None else round(v / 100.0, 4)
         k["stall_long_scoreboard"] = get("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio")
         cfg[key] = k
+    if work:
+        # the profiled frame's work counters (tools/frames.py output over the same
+        # frames): bench.py scales instructions per unit of work to its own frames
+        cfg["_work"] = {k: work[k] for k in ("pairs", "valid_texels", "node_visits") if k in work}
     data[config] = cfg
     with open(path, "w") as fh:
         json.dump(data, fh, indent=1, sort_keys=True)
@@ -155,12 +161,17 @@ def main():
     ap.add_argument("--tag", required=True)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--launches")
+    ap.add_argument("--frames-log", help="tools/frames.py output of the profiled command (work counters)")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     if a.launches:
         launches(a.launches, a.tag)
     if a.rep:
-        summarise(a.rep, a.tag, a.config)
+        work = None
+        if a.frames_log:
+            lines = [l for l in open(a.frames_log) if l.startswith("{")]
+            work = json.loads(lines[-1]) if lines else None
+        summarise(a.rep, a.tag, a.config, work)
 
 
 if __name__ == "__main__":
