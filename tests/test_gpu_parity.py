@@ -345,6 +345,12 @@ def test_benchmark_config_frame_parity(cuda, oracle, name, view):
     fr = render_frame(fc, g, t, RbfParams(sigma=cfg.sigma), cfg.settings(), debug=True)
     assert fr.visible
     _frame_vs_oracle(fr, oracle, fc, g)
+    # the production launch (launch list: only blocks that may see the mask polygon get
+    # a discretize CTA) renders the same frame as the debug launch (every block)
+    prod = render_frame(fc, g, t, RbfParams(sigma=cfg.sigma), cfg.settings())
+    assert np.array_equal(prod.pixels, fr.pixels)
+    assert (prod.visible_texels, prod.valid_texels, prod.rays_hit, prod.work) == \
+        (fr.visible_texels, fr.valid_texels, fr.rays_hit, fr.work)
     lays = [L for L in fr.debug["layouts"] if L is not None]
     assert len(lays) == cfg.cascades
     worst = 0.0
@@ -429,6 +435,8 @@ def test_random_pose_frame_parity(cuda, oracle, i):
     if not fr.visible:
         pytest.skip("nothing visible from this pose")
     _frame_vs_oracle(fr, oracle, fc, g)
+    prod = render_frame(fc, g, t, RbfParams(sigma=cfg.sigma), st)     # launch-list path
+    assert np.array_equal(prod.pixels, fr.pixels) and prod.work == fr.work
     print(f"pose {i}: K={st.count} R={st.resolution} rays_hit={fr.rays_hit}")
 
 
