@@ -183,7 +183,8 @@ class StripFrame:
     the upper mips, valid ranges and the strip's rays.  Pixels land in the frame
     buffers' `rgb[:, x0:x1]`."""
 
-    def __init__(self, config, grid, table, settings, rects, rank, slot=0, debug=False, events=None):
+    def __init__(self, config, grid, table, settings, rects, rank, slot=0, debug=False, events=None,
+                 staged=None):
         import torch
         from .render import prepare_frame
         self.rects, self.rank = rects, rank
@@ -192,11 +193,13 @@ class StripFrame:
         self.prep = prepare_frame(config, grid, table, settings, debug, slot)
         self.visible = self.prep is not None
         self.world = len(rects)
+        # one strip renders as a plain frame unless `staged` forces the exchange stages
+        self.staged = self.world > 1 if staged is None else bool(staged)
         if not self.visible:
             return
         self.buf, self.plan, self.plan_ms, self._launch = self.prep
         n = exchange_floats(settings)
-        if self.world > 1 and n == 0:
+        if self.staged and n == 0:
             raise ValueError("screen-strip sharding needs cascades of at least 66 texels")
         xb = getattr(self.buf, "_xchg", None)
         if xb is None or xb.numel() != n:
@@ -205,13 +208,13 @@ class StripFrame:
         self.footprint = strip_footprint(config.camera, config.width, config.height, rects, rank)
 
     def stage1(self):
-        if self.world == 1:          # a whole frame: no exchange
+        if not self.staged:          # a whole frame: no exchange
             self._launch(rect=self.rect, events=self.events)
         else:
             self._launch(rect=self.rect, events=self.events, stage=1, footprint=self.footprint, xchg=self.xchg)
 
     def stage2(self):
-        if self.world > 1:
+        if self.staged:
             self._launch(rect=self.rect, events=self.events, stage=2, footprint=self.footprint, xchg=self.xchg)
 
     def strip(self):
@@ -238,7 +241,7 @@ def render_strip(config, grid, table, params, settings, rect, rects=None, rank=N
     if not f.visible:
         return None
     f.stage1()
-    if f.world > 1:
+    if f.staged:
         reduce(f.xchg)
     f.stage2()
     return f.strip().clone()
@@ -256,7 +259,7 @@ def render_strips_one_gpu(config, grid, table, params, settings, world: int, rec
         return None, None
     for f in frames:
         f.stage1()
-    if world > 1:
+    if frames[0].staged:
         red = frames[0].xchg.clone()
         for f in frames[1:]:
             torch.maximum(red, f.xchg, out=red)

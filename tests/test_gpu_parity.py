@@ -612,3 +612,36 @@ def test_scalar_twins_match_reference(cuda):
                            else np.array([1, h.t, *h.uv, *h.patch]))
                     assert np.array_equal(got, want[i], equal_nan=True), (p, layer, k, i)
     assert n_hits > 3000 and n_blend > 100
+
+
+def test_nccl_exchange_and_gather_single_rank(cuda):
+    """The sharded frame's collectives on the NCCL backend (one rank on this GPU: the
+    only multi-GPU evidence one GPU can give): a sharded C2 strip frame whose exchange
+    buffer goes through dist.all_reduce(MAX) and whose image goes through
+    dist.gather equals the plain frame."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2201_10887_b200 import multi, render_frame
+    from paper_2201_10887_b200.rbf import RbfParams
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=cuda)
+    try:
+        cfg, g, t, fc = _config_inputs("C2")
+        P = RbfParams(sigma=cfg.sigma)
+        rects = [(0, fc.width)]
+        f = multi.StripFrame(fc, g, t, cfg.settings(), rects, 0, staged=True)
+        f.stage1()
+        before = f.xchg.clone()
+        multi.all_reduce_max(f.xchg)
+        assert torch.equal(before, f.xchg)           # one rank: MAX is the identity
+        f.stage2()
+        img = multi.gather_strips(f.strip().clone(), rects, 0, 1)
+        full = render_frame(fc, g, t, P, cfg.settings()).pixels
+        assert np.array_equal(img.cpu().numpy(), full)
+    finally:
+        dist.destroy_process_group()
