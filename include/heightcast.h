@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define HC_ABI_VERSION 5
+#define HC_ABI_VERSION 6
 #define HC_MAX_EDGES 32      /* polygon edges per cascade mask          */
 #define HC_MAX_CASCADES 8    /* K (the reference hard-codes 3)           */
 #define HC_MAX_LEVELS 20     /* max-mip levels (R <= 2^19)               */
@@ -362,6 +362,9 @@ typedef struct {
     int32_t *tile_cost;                  /* [hc_render_tiles(0,0,width,height)] */
     int32_t *tile_order;                 /* [hc_render_order_words(0,0,width,height)] */
     int32_t capacity, resolution, width, height;
+    int32_t throughput;                  /* nonzero: frames overlap (render_frames); the render runs
+                                          * its high-occupancy instantiation whatever the frame size */
+    int32_t reserved;
 } HcFrameBuffers;
 
 typedef struct {

@@ -17,7 +17,7 @@ LIB_DIR = os.path.join(PKG_DIR, "_lib")
 LIB_PATH = os.environ.get("HC_LIB_PATH") or os.path.join(LIB_DIR, "libheightcast_cuda.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 
-HC_ABI_VERSION = 5
+HC_ABI_VERSION = 6
 HC_MAX_EDGES = 32
 HC_MAX_CASCADES = 8
 HC_MAX_LEVELS = 20
@@ -123,7 +123,8 @@ class HcFrameBuffers(C.Structure):
     _fields_ = [("terrain", _vp), ("water", _vp), ("valid", _vp), ("mask", _vp), ("patch_ok", _vp),
                 ("mip", _vp), ("vrange", _vp), ("mip_ws", _vp), ("mip_ws_bytes", C.c_size_t), ("rgb", _vp),
                 ("counters", _vp), ("tile_counter", _vp), ("tile_cost", _vp), ("tile_order", _vp),
-                ("capacity", _i32), ("resolution", _i32), ("width", _i32), ("height", _i32)]
+                ("capacity", _i32), ("resolution", _i32), ("width", _i32), ("height", _i32),
+                ("throughput", _i32), ("reserved", _i32)]
 
 
 class HcFootprint(C.Structure):

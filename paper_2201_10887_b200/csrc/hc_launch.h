@@ -45,6 +45,7 @@ int maxmip_top_launch(const HcMipJob* jobs, int n_jobs, float* partial, int part
 int maxmip_launch(const HcMipJob* jobs, int n_jobs, void* workspace, size_t workspace_bytes, const OrderJob* ord,
                   cudaStream_t stream);
 // order_ready: the tile order (and queue head) were produced by maxmip_launch
-int render_launch(const HcRenderArgs* args, bool order_ready, cudaStream_t stream);
+// throughput: frames overlap on the GPU, use the high-occupancy render instantiation
+int render_launch(const HcRenderArgs* args, bool order_ready, cudaStream_t stream, bool throughput = false);
 
 }  // namespace hc

@@ -848,7 +848,7 @@ static int frame_launch(int stages, const HcPlan* plan, const HcCamera* cam, con
         int rc = hc::maxmip_top_launch(jobs, 2 * K, dm.partial, dm.partial_slots, side, &ord, s, xchg);
         if (rc) return rc;
         rec(2);
-        rc = hc::render_launch(&A, A.tile_order != nullptr, s);
+        rc = hc::render_launch(&A, A.tile_order != nullptr, s, buf->throughput != 0);
         if (rc) return rc;
         rec(3);
     }

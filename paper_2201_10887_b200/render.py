@@ -173,13 +173,13 @@ def _shading(config):
 
 def enqueue_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable,
                   settings: CascadeSettings = CascadeSettings(), debug: bool = False, rect=None, events=None,
-                  slot: int = 0):
+                  slot: int = 0, throughput: bool = False):
     """Plan natively on the host and enqueue one frame's kernels on the current stream.
 
     Returns (buffers, plan, plan_ms) without waiting for the GPU, or None when
     nothing is visible.  The device-resident half of `render_frame`; pixels stay
     in `buffers.rgb` until read back."""
-    prep = prepare_frame(config, grid, table, settings, debug, slot)
+    prep = prepare_frame(config, grid, table, settings, debug, slot, throughput)
     if prep is None:
         return None
     buf, plan, plan_ms, launch = prep
@@ -188,10 +188,13 @@ def enqueue_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable
 
 
 def prepare_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable,
-                  settings: CascadeSettings = CascadeSettings(), debug: bool = False, slot: int = 0):
+                  settings: CascadeSettings = CascadeSettings(), debug: bool = False, slot: int = 0,
+                  throughput: bool = False):
     """Plan one frame on the host and bind its buffer set: (buffers, plan, plan_ms,
     launch) or None when nothing is visible; `launch(**kw)` enqueues the frame (or
-    one stage of a sharded frame, see multi.py) via _engine.launch_planned."""
+    one stage of a sharded frame, see multi.py) via _engine.launch_planned.
+    `throughput`: the frame overlaps other frames on the GPU (render_frames), so the
+    render uses its high-occupancy instantiation (hc_render.cu)."""
     tp = time.perf_counter()
     plan = plan_native(config.camera, grid, settings.resolution, settings.overlap, settings.count)
     if plan.status != 0:
@@ -201,6 +204,7 @@ def prepare_frame(config: FrameConfig, grid: AdaptiveGrid, table: InfluenceTable
     ginf = gdev.influence(table)
     buf = _frame_buffers(gdev.device, settings.count, settings.resolution, config.width, config.height, debug,
                          slot)
+    buf.native.throughput = 1 if throughput else 0
     dom = getattr(grid, "_hc_domain", None)
     if dom is None:
         dom = grid._hc_domain = _cascade_domain(grid)
@@ -280,7 +284,7 @@ def render_frames(configs, grid: AdaptiveGrid, table: InfluenceTable, params: Rb
                         before_frame(i)
                     if read_done[slot] is not None:
                         compute.wait_event(read_done[slot])  # slot's previous pixels copied out
-                    queued = enqueue_frame(config, grid, table, settings, slot=slot)
+                    queued = enqueue_frame(config, grid, table, settings, slot=slot, throughput=depth > 1)
                 if queued is None:
                     pending.append(("background", config))
                 else:
