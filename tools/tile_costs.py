@@ -19,6 +19,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C2")
     ap.add_argument("--frames", type=int, default=5)
+    ap.add_argument("--path", type=int, default=0,
+                    help="instead: N poses of the bench camera path, render ms vs max tile cost per pose")
     a = ap.parse_args()
     import torch
     from paper_2201_10887_b200 import build_influence_table
@@ -28,6 +30,19 @@ def main():
     g = cfg.grid()
     t = build_influence_table(g, cfg.sigma)
     fc, st = cfg.frame_config(), cfg.settings()
+    if a.path:
+        for i in range(0, 2 * 60, max(1, 120 // a.path)):
+            pc = cfg.path_frame_config(i)
+            rr = []
+            for _ in range(3):        # the third launch orders its queue from the same pose
+                buf, _p, _ms = enqueue_frame(pc, g, t, st)
+                buf.ev[2].synchronize()
+                rr.append(buf.ev[4].elapsed_time(buf.ev[2]))
+            cost = buf.tile_cost.cpu().numpy()
+            cnt = buf.counters.cpu().numpy()
+            print(f"pose {i}: render {rr[-1]:.3f} ms, max tile {int(cost.max())}, top8 {np.sort(cost)[-8:][::-1].tolist()}, "
+                  f"visits {cnt[5]}, sum tile max {int(cost.sum())}", flush=True)
+        return
     r = []
     for _ in range(a.frames):
         buf, _p, _ms = enqueue_frame(fc, g, t, st)
