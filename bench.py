@@ -353,15 +353,16 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # strips: cut from the ranks' measured frame times (multi.StripSequence)
+    seq_strips = multi.StripSequence(cfg.width, ws, rank) if strips and ws > 1 else None
+
     def step(i, events=None):
-        if strips and ws > 1:
+        if seq_strips is not None:
             # sharded strip: footprint discretization, the one MAX all-reduce of the
-            # mip exchange buffer (between events 1 and 2), upper mips + the strip's rays
-            f = multi.StripFrame(frame_of(i), g, table, st, rects, rank, events=events)
-            f.stage1()
-            multi.all_reduce_max(f.xchg)
-            f.stage2()
-            return f.buf, f.plan, f.plan_ms
+            # mip exchange buffer and frame times (between events 1 and 2), upper mips +
+            # the strip's rays
+            f = seq_strips.frame(frame_of(i), g, table, st, events=events)
+            return (f.buf, f.plan, f.plan_ms) if f.visible else None
         return enqueue_frame(frame_of(i), g, table, st, rect=rect, events=events)
 
     # ---- warm-up (device-resident path): the last warm-up poses of the path, so the
@@ -432,8 +433,10 @@ def main():
         e2e_ms = [(time.perf_counter() - t0) * 1e3]
     else:
         def e2e_step(i):
-            part = multi.render_strip(frame_of(i), g, table, P, st, rects[rank], rects=rects, rank=rank)
-            img = multi.gather_strips(part, rects, rank, ws) if ws > 1 else part
+            f = seq_strips.frame(frame_of(i), g, table, st)
+            if not f.visible:
+                return
+            img = multi.gather_strips(f.strip().clone(), f.rects, rank, ws)
             if rank == 0:
                 img.cpu()
 

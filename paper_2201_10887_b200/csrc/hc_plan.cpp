@@ -797,9 +797,11 @@ static int frame_launch(int stages, const HcPlan* plan, const HcCamera* cam, con
     A.rgb = buf->rgb;
     A.counters = buf->counters;
     A.tile_counter = buf->tile_counter;
-    const bool full = !rect || (A.x0 == 0 && A.y0 == 0 && A.x1 == buf->width && A.y1 == buf->height);
-    A.tile_cost = full ? buf->tile_cost : nullptr;
-    A.tile_order = full ? buf->tile_order : nullptr;
+    // heaviest-first tile queue from the previous launch's per-tile costs, for strips
+    // too (tiles numbered within the rectangle; when the strip's cuts move, the stale
+    // costs only make the order less good -- order never changes results)
+    A.tile_cost = buf->tile_cost;
+    A.tile_order = buf->tile_order;
     if (dbg) A.dbg = *dbg;
 
     if ((stages & 1) && buf->counters &&

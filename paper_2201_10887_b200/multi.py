@@ -91,6 +91,43 @@ def gather_strips(strip: "torch.Tensor", rects, rank: int, world: int, group=Non
     return out
 
 
+class StripBalancer:
+    """Cost-balanced screen strips from measured per-rank frame times.
+
+    A strip's cost is modelled as uniform over its columns (its time / its width);
+    the next cuts split the image at equal modelled cost (`screen_strips` with
+    per-column weights), moved only `damping` of the way from the old cuts so they
+    do not oscillate while the view moves, and kept at least `min_width` pixels
+    apart.  Every rank feeds the same times (exchanged in the frame's all-reduce, see
+    `StripFrame.times_slot`), so every rank computes the same cuts."""
+
+    def __init__(self, width: int, world: int, damping: float = 0.7, min_width: int = 4 * TILE_W):
+        self.width, self.world, self.damping = width, world, damping
+        self.min_width = min(min_width, max(TILE_W, width // max(world, 1) // TILE_W * TILE_W))
+        self.rects = screen_strips(width, world)
+
+    def update(self, times):
+        t = np.asarray(times, dtype=np.float64)
+        if self.world < 2 or len(t) != self.world or not np.all(np.isfinite(t)) or np.any(t <= 0):
+            return self.rects
+        cols = np.empty(self.width)
+        for (x0, x1), ti in zip(self.rects, t):
+            cols[x0:x1] = ti / max(x1 - x0, 1)
+        target = screen_strips(self.width, self.world, cols)
+        old = [x0 for x0, _ in self.rects] + [self.width]
+        new = [x0 for x0, _ in target] + [self.width]
+        cuts = [0]
+        for r in range(1, self.world):
+            c = (1.0 - self.damping) * old[r] + self.damping * new[r]
+            c = TILE_W * int(round(c / TILE_W))
+            lo = cuts[-1] + self.min_width
+            hi = self.width - (self.world - r) * self.min_width
+            cuts.append(min(max(c, lo), hi))
+        cuts.append(self.width)
+        self.rects = [(cuts[r], cuts[r + 1]) for r in range(self.world)]
+        return self.rects
+
+
 FOOTPRINT_MARGIN = 2.5        # texels of dilation of a block's square (SURVEY.md §8 e)
 _WIDEN = 1e-9                  # radians: each wedge boundary turned outward
 
@@ -201,10 +238,14 @@ class StripFrame:
         n = exchange_floats(settings)
         if self.staged and n == 0:
             raise ValueError("screen-strip sharding needs cascades of at least 66 texels")
+        # the exchange buffer, plus one float per rank after it: each rank's last
+        # measured frame time rides in the same MAX all-reduce (StripBalancer input)
+        total = n + _cuda_max_strips()
         xb = getattr(self.buf, "_xchg", None)
-        if xb is None or xb.numel() != n:
-            xb = self.buf._xchg = torch.empty(max(n, 1), dtype=torch.float32, device=self.buf.rgb.device)
+        if xb is None or xb.numel() != total:
+            xb = self.buf._xchg = torch.zeros(total, dtype=torch.float32, device=self.buf.rgb.device)
         self.xchg = xb
+        self.times_slot = xb[n:n + self.world]
         self.footprint = strip_footprint(config.camera, config.width, config.height, rects, rank)
 
     def stage1(self):
@@ -220,6 +261,71 @@ class StripFrame:
     def strip(self):
         x0, _, x1, _ = self.rect
         return self.buf.rgb[:, x0:x1]
+
+
+class StripSequence:
+    """This rank's screen strips of a sequence of frames (a camera path), with the
+    strips rebalanced from the ranks' measured frame times.
+
+    Each rank writes the time of its newest completed frame into the exchange
+    buffer's time slots, which ride in the frame's one MAX all-reduce; step i cuts
+    the image with the times exchanged at step i - LAG, so every rank changes its
+    cuts at the same step and none waits on a frame still in flight.  With one rank
+    the frame is a plain full frame."""
+
+    LAG = 2
+
+    def __init__(self, width: int, world: int, rank: int, balance: bool = True):
+        self.world, self.rank, self.balance = world, rank, balance and world > 1
+        self.balancer = StripBalancer(width, world)
+        self._pending = {}
+        self._own = []
+        self._last_ms = 0.0
+        self._step = 0
+
+    @property
+    def rects(self):
+        return self.balancer.rects
+
+    def frame(self, config, grid, table, settings, events=None, reduce=all_reduce_max):
+        """Enqueue this rank's strip of `config` (both stages and the exchange);
+        returns the StripFrame (pixels in `frame.strip()` once the stream gets there)."""
+        import torch
+        i = self._step
+        self._step += 1
+        if self.balance and (i - self.LAG) in self._pending:
+            ev, host = self._pending.pop(i - self.LAG)
+            ev.synchronize()
+            self.balancer.update(host.numpy())
+        while self._own and self._own[0][1].query():
+            e0, e1 = self._own.pop(0)
+            self._last_ms = e0.elapsed_time(e1)
+        f = StripFrame(config, grid, table, settings, self.balancer.rects, self.rank, events=events)
+        if not f.visible:
+            return f
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        f.stage1()
+        if f.staged:
+            f.times_slot.zero_()
+            f.times_slot[self.rank:self.rank + 1].fill_(self._last_ms)
+            reduce(f.xchg)
+            if self.balance:
+                host = torch.empty(self.world, dtype=torch.float32, pin_memory=True)
+                host.copy_(f.times_slot, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record()
+                self._pending[i] = (ev, host)
+        f.stage2()
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        self._own.append((e0, e1))
+        return f
+
+
+def _cuda_max_strips() -> int:
+    from . import _cuda
+    return _cuda.HC_MAX_STRIPS
 
 
 def render_strip(config, grid, table, params, settings, rect, rects=None, rank=None, reduce=all_reduce_max):

@@ -152,3 +152,31 @@ def test_strip_wedge_of_full_width_view_is_the_view():
     assert not whole
     a0, a1 = math.atan2(d0[1], d0[0]), math.atan2(d1[1], d1[0])
     assert a0 < 0 < a1 and abs(a0 + a1) < 1e-6
+
+
+def test_strip_balancer_converges_on_uneven_cost():
+    """Strips cut from measured per-rank times converge to equal cost on a cost
+    profile with a heavy band (the horizon's long rays), cuts snapped to tiles and at
+    least min_width apart, identical for identical inputs (every rank computes them)."""
+    W, world = 3840, 8
+    x = np.arange(W) + 0.5
+    density = 1.0 + 30.0 * np.exp(-((x - 2100.0) / 250.0) ** 2)
+    bal = multi.StripBalancer(W, world)
+    cost = lambda rects: np.array([density[a:b].sum() for a, b in rects])
+    first = cost(bal.rects)
+    for _ in range(12):
+        bal.update(cost(bal.rects))
+    last = cost(bal.rects)
+    assert last.max() / last.mean() < 0.6 * (first.max() / first.mean())
+    assert last.max() / last.mean() < 1.35
+    xs = [a for a, _ in bal.rects] + [W]
+    assert xs[0] == 0 and xs[-1] == W
+    assert all(b - a >= bal.min_width for a, b in bal.rects)
+    assert all(a % multi.TILE_W == 0 for a, _ in bal.rects)
+    twin = multi.StripBalancer(W, world)
+    for _ in range(12):
+        twin.update(cost(twin.rects))
+    assert twin.rects == bal.rects
+    # missing / invalid measurements leave the cuts alone
+    before = list(bal.rects)
+    assert bal.update([0.0] * world) == before and bal.update([1.0] * (world - 1)) == before

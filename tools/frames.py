@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--frames", type=int, default=8)
     ap.add_argument("--start", type=int, default=0)
+    ap.add_argument("--balance", action="store_true", help="with --strips: rebalance cuts from per-rank times")
     ap.add_argument("--strips", default="",
                     help="emulate N sharded screen-strip ranks on this GPU: per-rank stage-1 "
                          "(footprint discretization) and stage-2 (mips + strip render) event times")
@@ -36,9 +37,14 @@ def main():
     mk = lambda: torch.cuda.Event(enable_timing=True)
     for n_strips in [int(x) for x in a.strips.split(",") if x]:
         from paper_2201_10887_b200 import multi
-        rects = multi.screen_strips(cfg.width, n_strips)
+        bal = multi.StripBalancer(cfg.width, n_strips)
+        rects = bal.rects
         rows = []
         for i in range(a.frames):
+            if a.balance and rows:
+                # every rank's time of the previous frame (in a real run: exchanged in the
+                # frame's all-reduce, used LAG frames later)
+                rects = bal.update([d + r for d, r, _ in rows[-1]])
             fc = cfg.path_frame_config(a.start + i)
             evs = [[mk() for _ in range(4)] for _ in rects]
             for e4 in evs:
@@ -60,7 +66,9 @@ def main():
             rows.append([(e[0].elapsed_time(e[1]), e[2].elapsed_time(e[3]),
                           int(f.buf.counters[_cuda.CNT_PAIRS])) for e, f in zip(evs, fr)])
         mean = lambda xs: sum(xs) / len(xs)
-        out = {"strips": n_strips, "rects": rects,
+        per = [max(d + r for d, r, _ in row) for row in rows]
+        out = {"strips": n_strips, "balanced": bool(a.balance), "rects": rects,
+               "max_rank_ms_per_frame": [round(x, 4) for x in per],
                "discretize_ms": [round(mean([r[k][0] for r in rows]), 4) for k in range(n_strips)],
                "render_ms": [round(mean([r[k][1] for r in rows]), 4) for k in range(n_strips)],
                "pairs": [mean([r[k][2] for r in rows]) for k in range(n_strips)]}
