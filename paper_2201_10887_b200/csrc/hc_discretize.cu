@@ -1017,7 +1017,7 @@ int hc::discretize_launch(const HcCascadeRaster* cascades, int n_cascades, const
         P.partial = mips->partial;
         P.full_mips = mips->full;
         if (mips->xchg) {
-            HC_REQUIRE(mips->fp && mips->n_levels >= 7, "hc_frame_stage: sharding needs a footprint and R >= 66");
+            HC_REQUIRE(mips->fp && mips->n_levels >= 7, "hc_frame_stage: sharding needs a footprint and R >= 34");
             HC_REQUIRE(mips->fp->n_strips >= 1 && mips->fp->n_strips <= HC_MAX_STRIPS && mips->fp->rank >= 0 &&
                            mips->fp->rank < mips->fp->n_strips,
                        "hc_frame_stage: bad footprint (%d strips, rank %d)", mips->fp->n_strips, mips->fp->rank);

@@ -237,7 +237,7 @@ class StripFrame:
         self.buf, self.plan, self.plan_ms, self._launch = self.prep
         n = exchange_floats(settings)
         if self.staged and n == 0:
-            raise ValueError("screen-strip sharding needs cascades of at least 66 texels")
+            raise ValueError("screen-strip sharding needs cascades of at least 34 texels (7 mip levels)")
         # the exchange buffer, plus one float per rank after it: each rank's last
         # measured frame time rides in the same MAX all-reduce (StripBalancer input)
         total = n + _cuda_max_strips()

@@ -440,10 +440,13 @@ def test_random_pose_frame_parity(cuda, oracle, i):
     print(f"pose {i}: K={st.count} R={st.resolution} rays_hit={fr.rays_hit}")
 
 
-@pytest.mark.parametrize("R,K,overlap", [(300, 2, 5.0), (1000, 3, "auto"), (129, 5, 0.0), (777, 8, 12.5)])
+@pytest.mark.parametrize("R,K,overlap", [(300, 2, 5.0), (1000, 3, "auto"), (129, 5, 0.0), (777, 8, 12.5),
+                                         (4, 1, 0.0), (5, 2, "auto"), (33, 3, 1.0), (65, 2, "auto"),
+                                         (4096, 2, "auto")])
 def test_odd_resolution_frame_parity(cuda, oracle, R, K, overlap):
     """Non-power-of-two cascade resolutions (odd pyramid widths, -inf padding, partial
-    CTA tiles in every kernel), explicit overlaps and up to 8 cascades: bit-exact ray
+    CTA tiles in every kernel), explicit overlaps and up to 8 cascades, down to the
+    reference's minimum R = 4 (cascade.py:454) and up to 4096^2 cascades: bit-exact ray
     casting on the GPU's rasters, exact masks/valid bits, heights within tolerance."""
     from paper_2201_10887_b200 import render_frame
     from paper_2201_10887_b200.rbf import RbfParams
@@ -459,6 +462,22 @@ def test_odd_resolution_frame_parity(cuda, oracle, R, K, overlap):
         assert np.array_equal(valid, o.valid) and np.array_equal(_np(L.mask), o.mask)
         for layer in ("terrain", "water"):
             _check_heights(_np(r.layer(layer)), o.layer(layer), valid, f"R={R} {layer}")
+
+
+def test_sharded_strips_need_six_mip_levels(cuda):
+    """Screen-strip sharding exchanges level-5 mip nodes, so it needs 7 mip levels,
+    R >= 34 (hc_frame_xchg_floats == 0 below); a smaller raster is refused, not
+    mis-rendered, and the smallest allowed one renders bit-identical strips."""
+    from paper_2201_10887_b200 import multi
+    from paper_2201_10887_b200.render import CascadeSettings
+    cfg, g, t, fc = _config_inputs("C2", 480, 300)
+    with pytest.raises(ValueError, match="at least 34"):
+        multi.StripFrame(fc, g, t, CascadeSettings(resolution=33, count=2), multi.screen_strips(480, 2), 0)
+    img, _ = multi.render_strips_one_gpu(fc, g, t, None, CascadeSettings(resolution=34, count=2), 2)
+    from paper_2201_10887_b200 import render_frame
+    from paper_2201_10887_b200.rbf import RbfParams
+    full = render_frame(fc, g, t, RbfParams(sigma=cfg.sigma), CascadeSettings(resolution=34, count=2)).pixels
+    assert np.array_equal(img, full)
 
 
 def test_division_selftest(cuda):
