@@ -10,7 +10,7 @@
 //   raycast.py:61-88        max-mip levels 0..5 (fused epilogue, frame launches)
 //   discretize.py:44-49     valid height range (per-CTA partials)
 //
-// Design (B200).  One CTA per 32x32 texel block of a cascade, 8 warps.
+// Design (B200).  One CTA per 32x32 texel block of a cascade, 6 warps, 3 CTAs per SM.
 //  1. Classification: warp 0 tests the block's corner box against the mask
 //     polygon (classify_block); a block provably outside writes sentinels (and
 //     sentinel mips) and leaves; a block provably inside skips the per-texel
@@ -55,12 +55,9 @@ constexpr double NEG_HALF_LOG2E = -0.72134752044448170368;
 // r2 >= 12.25 (3.5 sigma, rbf.py:29-32) <=> q = r2 * NEG_HALF_LOG2E <= Q_CUT
 constexpr float Q_CUT = (float)(12.25 * NEG_HALF_LOG2E);
 #ifndef DISC_STAGE_PAIRS
-#define DISC_STAGE_PAIRS 96        // 2 CTAs per SM, ~85 KB shared memory each (the rest of the 256 KB
-                                   // stays L1 for the lookups and gathers); measured 32-128 / 2-3 CTAs
-                                   // per SM: 96 best
-#endif
-#ifndef DISC_MIN_CTAS
-#define DISC_MIN_CTAS 2
+#define DISC_STAGE_PAIRS 80        // record pairs per warp buffer: ~64 KB shared memory per 6-warp CTA
+                                   // (3 per SM), the rest of the 256 KB stays L1 for the lookups and
+                                   // gathers (measured 32-128 pairs at 4/5/6/8 warps: DESIGN.md §4)
 #endif
 constexpr int STAGE_PAIRS = DISC_STAGE_PAIRS;   // record pairs per warp buffer, shared by up to STAGE_GROUPS cells
 #ifndef DISC_GATHER_PREFETCH
@@ -70,7 +67,18 @@ constexpr int STAGE_PAIRS = DISC_STAGE_PAIRS;   // record pairs per warp buffer,
 #define DISC_STAGE_GROUPS 12       // cells per staged unit (8 / 12 / 16 measured: 12 best)
 #endif
 constexpr int STAGE_GROUPS = DISC_STAGE_GROUPS;
-constexpr int DISC_WARPS = 8;
+// Two CTA shapes (the same 32x32 blocks, the same per-texel arithmetic and results):
+//  * 6 warps, 3 CTAs per SM -- while one CTA waits at a barrier for its longest unit
+//    two others issue: 5-8 % faster on the 4K configs (32k blocks) and for
+//    overlapping frames (render_frames);
+//  * 8 warps, 2 CTAs per SM -- faster for a lone frame of a few thousand blocks (C1,
+//    C2), whose last wave of CTAs sets the time.
+#ifndef DISC_WIDE_BLOCKS
+#define DISC_WIDE_BLOCKS 16384     // blocks per launch from which the 6-warp shape is used
+#endif
+constexpr int MINB_FOR(int warps) { return warps == 6 ? 3 : 2; }
+// threads of an extra CTA that count a tile-queue histogram chunk (a divisor of ORDER_CHUNK)
+constexpr int ORDER_THREADS_FOR(int threads) { return threads >= 256 ? 256 : (threads >= 128 ? 128 : 64); }
 constexpr int BLK = 32;            // texels per block side (= level-5 mip node)
 constexpr int TILE_LEVELS = 6;     // mip levels 0..5 reduced per block
 constexpr int QUAD = 10;           // float4 per quad of record pairs (heightcast.h HcGrid.rec)
@@ -428,18 +436,20 @@ __device__ __forceinline__ float* partial_slot(const DiscParams& P, int kc, int 
     return P.xchg ? P.xchg + (int64_t)2 * P.n_cascades * P.l5_nodes + slot : P.partial + slot;
 }
 
-template <bool MIPS>
-__global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_constant__ DiscParams P,
+template <bool MIPS, int DISC_WARPS>
+__global__ void __launch_bounds__(DISC_WARPS * 32, MINB_FOR(DISC_WARPS)) k_discretize(const __grid_constant__ DiscParams P,
                                                        const __grid_constant__ HcGrid g) {
     constexpr int REG = MIPS ? BLK + 1 : BLK;      // region side (block + halo)
     constexpr int NT = REG * REG;
     constexpr int NU = MIPS ? 35 : 32;             // units of 32 texels
+    constexpr int DISC_THREADS = DISC_WARPS * 32;
+    constexpr int ORDER_THREADS = ORDER_THREADS_FOR(DISC_THREADS);
     const unsigned FULL = 0xffffffffu;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     if ((int)blockIdx.x >= P.n_blocks) {           // tile-queue order: one histogram chunk per CTA
         const int chunk = (int)blockIdx.x - P.n_blocks;
-        if (chunk < order_chunks(P.ord.n_tiles)) order_count_chunk<256>(P.ord.cost, P.ord.order, P.ord.n_tiles, chunk);
+        if (chunk < order_chunks(P.ord.n_tiles)) order_count_chunk<ORDER_THREADS>(P.ord.cost, P.ord.order, P.ord.n_tiles, chunk);
         return;
     }
     const int bs = P.blocks_side;
@@ -493,17 +503,19 @@ __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_
     const bool vec4 = (R & 3) == 0 && bx + BLK <= R;
     if (cls == 0) {        // the whole region lies outside the mask polygon
         if (vec4) {
-            const int y = by + (tid >> 3), x = bx + 4 * (tid & 7);
-            if (y < R) {
-                const int64_t o = (int64_t)y * R + x;
-                const float4 sv = make_float4(sentinel, sentinel, sentinel, sentinel);
-                *reinterpret_cast<float4*>(c.terrain + o) = sv;
-                *reinterpret_cast<float4*>(c.water + o) = sv;
-                *reinterpret_cast<uint32_t*>(c.valid + o) = 0u;
-                if (c.mask) *reinterpret_cast<uint32_t*>(c.mask + o) = 0u;
+            for (int yy = tid >> 3; yy < BLK; yy += DISC_THREADS / 8) {
+                const int y = by + yy, x = bx + 4 * (tid & 7);
+                if (y < R) {
+                    const int64_t o = (int64_t)y * R + x;
+                    const float4 sv = make_float4(sentinel, sentinel, sentinel, sentinel);
+                    *reinterpret_cast<float4*>(c.terrain + o) = sv;
+                    *reinterpret_cast<float4*>(c.water + o) = sv;
+                    *reinterpret_cast<uint32_t*>(c.valid + o) = 0u;
+                    if (c.mask) *reinterpret_cast<uint32_t*>(c.mask + o) = 0u;
+                }
             }
         } else {
-            for (int e = tid; e < BLK * BLK; e += 256) {
+            for (int e = tid; e < BLK * BLK; e += DISC_THREADS) {
                 const int x = bx + (e & 31), y = by + (e >> 5);
                 if (x < R && y < R) {
                     const int64_t o = (int64_t)y * R + x;
@@ -525,7 +537,7 @@ __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_
             // k_render (it recomputes level-0 maxima from the corners); it is written
             // when the caller inspects the whole pyramid (debug frames).
             if (!P.full_mips && P.patch_ok[kc]) {
-                for (int e = tid; e < BLK * BLK; e += 256) {
+                for (int e = tid; e < BLK * BLK; e += DISC_THREADS) {
                     const int gx = bx + (e & 31), gy = by + (e >> 5);
                     if (gx < n0 && gy < n0) P.patch_ok[kc][(int64_t)gy * n0 + gx] = 0;
                 }
@@ -536,7 +548,7 @@ __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_
                 if (L < L0) continue;
                 if (L >= P.n_levels) break;
                 const int side = BLK >> L, wl = P.level_w[L];
-                for (int e = tid; e < side * side; e += 256) {
+                for (int e = tid; e < side * side; e += DISC_THREADS) {
                     const int gx = (bx >> L) + e % side, gy = (by >> L) + e / side;
                     if (gx < wl && gy < wl) {
                         const int64_t o = P.level_off[L] + (int64_t)gy * wl + gx;
@@ -560,13 +572,14 @@ __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_
     }
 
     // ---- 2. per-texel mask, cell lookup and record range (all dependent loads here)
-    {
-        constexpr int PER = (NT + 255) / 256;
+#pragma unroll 1
+    for (int pass0 = 0; pass0 < NT; pass0 += 5 * DISC_THREADS) {
+        constexpr int PER = 5;               // texels per thread per pass (their loads in flight together)
         int cell[PER];
         double pxs[PER], pys[PER];
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
-            const int e = tid + 256 * i;
+            const int e = pass0 + tid + DISC_THREADS * i;
             cell[i] = -1;
             pxs[i] = pys[i] = 0.0;
             if (e < NT) {
@@ -582,7 +595,7 @@ __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_
         }
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
-            const int e = tid + 256 * i;
+            const int e = pass0 + tid + DISC_THREADS * i;
             if (e < NT) {
                 const int a = cell[i];
                 int2 pr = make_int2(0, 0);
@@ -748,7 +761,8 @@ __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_
         }
     };
     if (vec4) {
-        const int ty = tid >> 3, tx = 4 * (tid & 7);
+      for (int ty = tid >> 3; ty < BLK; ty += DISC_THREADS / 8) {
+        const int tx = 4 * (tid & 7);
         const int y = by + ty;
         if (y < R) {
             const int r = ty * REG + tx;
@@ -769,8 +783,9 @@ __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_
                 *reinterpret_cast<uint32_t*>(c.mask + o) =
                     (f[0] & 1u) | ((f[1] & 1u) << 8) | ((f[2] & 1u) << 16) | ((f[3] & 1u) << 24);
         }
+      }
     } else {
-        for (int e = tid; e < BLK * BLK; e += 256) {
+        for (int e = tid; e < BLK * BLK; e += DISC_THREADS) {
             const int tx = e & 31, ty = e >> 5;
             const int x = bx + tx, y = by + ty;
             if (x < R && y < R) {
@@ -803,7 +818,7 @@ __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_
 
     // level 0 (max of each patch's four corners, raycast.py:71-76) + patch bytes
     float* lv = reinterpret_cast<float*>(s_stage);             // [2][BLK][BLK + 1] (the staging area is idle)
-    for (int e = tid; e < BLK * BLK; e += 256) {
+    for (int e = tid; e < BLK * BLK; e += DISC_THREADS) {
         const int tx = e & 31, ty = e >> 5;
         const int gx = bx + tx, gy = by + ty;
         float m0 = -INFINITY, m1 = -INFINITY;
@@ -824,29 +839,27 @@ __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_
         lv[BLK * (BLK + 1) + ty * (BLK + 1) + tx] = m1;
     }
     __syncthreads();
-    // levels 1..5 in place: after level L, lv[.][y][x] for y, x < BLK >> L holds level L
+    // levels 1..5, ping-ponging between lv and a second area of the idle staging
+    // buffers: level L (side x side nodes, row stride BLK + 1) from level L - 1
+    float* lv2 = lv + 2 * BLK * (BLK + 1);
 #pragma unroll
     for (int L = 1; L < TILE_LEVELS; ++L) {              // unrolled: side is a constant
         if (L >= P.n_levels) break;
         const int side = BLK >> L;
         const int wl = P.level_w[L];
-        float m0 = 0.f, m1 = 0.f;
-        int y = 0, x = 0;
-        if (tid < side * side) {
-            y = tid / side;
-            x = tid % side;
-            const float* l0 = lv;
-            const float* l1 = lv + BLK * (BLK + 1);
-            const int s = BLK + 1;
-            m0 = fmaxf(fmaxf(l0[2 * y * s + 2 * x], l0[2 * y * s + 2 * x + 1]),
-                       fmaxf(l0[(2 * y + 1) * s + 2 * x], l0[(2 * y + 1) * s + 2 * x + 1]));
-            m1 = fmaxf(fmaxf(l1[2 * y * s + 2 * x], l1[2 * y * s + 2 * x + 1]),
-                       fmaxf(l1[(2 * y + 1) * s + 2 * x], l1[(2 * y + 1) * s + 2 * x + 1]));
-        }
-        __syncthreads();
-        if (tid < side * side) {
-            lv[y * (BLK + 1) + x] = m0;
-            lv[BLK * (BLK + 1) + y * (BLK + 1) + x] = m1;
+        const float* src = (L & 1) ? lv : lv2;
+        float* dst = (L & 1) ? lv2 : lv;
+        constexpr int s = BLK + 1;
+        for (int e = tid; e < side * side; e += DISC_THREADS) {
+            const int y = e / side, x = e % side;
+            const float* l0 = src;
+            const float* l1 = src + BLK * (BLK + 1);
+            const float m0 = fmaxf(fmaxf(l0[2 * y * s + 2 * x], l0[2 * y * s + 2 * x + 1]),
+                                   fmaxf(l0[(2 * y + 1) * s + 2 * x], l0[(2 * y + 1) * s + 2 * x + 1]));
+            const float m1 = fmaxf(fmaxf(l1[2 * y * s + 2 * x], l1[2 * y * s + 2 * x + 1]),
+                                   fmaxf(l1[(2 * y + 1) * s + 2 * x], l1[(2 * y + 1) * s + 2 * x + 1]));
+            dst[y * s + x] = m0;
+            dst[BLK * (BLK + 1) + y * s + x] = m1;
             const int gy = (by >> L) + y, gx = (bx >> L) + x;
             if (gx < wl && gy < wl) {
                 const int64_t o = P.level_off[L] + (int64_t)gy * wl + gx;
@@ -885,7 +898,7 @@ __global__ void __launch_bounds__(256, DISC_MIN_CTAS) k_discretize(const __grid_
     }
 }
 
-template <bool MIPS>
+template <bool MIPS, int DISC_WARPS>
 constexpr size_t disc_smem_bytes() {
     constexpr size_t REG = MIPS ? BLK + 1 : BLK;
     constexpr size_t NT = REG * REG;
@@ -893,7 +906,7 @@ constexpr size_t disc_smem_bytes() {
     constexpr size_t stage = DISC_WARPS * 2 * 16 * STAGE_F4 + DISC_WARPS * 2 * 8;
     return head + stage;
 }
-static_assert(DISC_WARPS * 2 * 16 * STAGE_F4 >= 2 * BLK * (BLK + 1) * 4, "mip levels alias the staging area");
+static_assert(6 * 2 * 16 * STAGE_F4 >= 2 * 2 * BLK * (BLK + 1) * 4, "mip levels alias the staging area");
 constexpr bool stage_fits() {
     for (int ng = 1; ng <= STAGE_GROUPS; ++ng)
         if (ng * (group_chunk(ng) / 4 * QUAD + 1) > STAGE_F4 || group_chunk(ng) < 4) return false;
@@ -967,6 +980,17 @@ extern "C" int hc_visibility_mask(const HcCascadeRaster* c, hc_stream_t stream) 
     return cuda_status("hc_visibility_mask");
 }
 
+template <bool MIPS, int W>
+static void launch_disc(const DiscParams& P, const HcGrid& g, int ctas, cudaStream_t stream) {
+    constexpr size_t smem = disc_smem_bytes<MIPS, W>();
+    static bool attr = false;          // per process; the attribute is per function
+    if (!attr) {
+        cudaFuncSetAttribute(k_discretize<MIPS, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    k_discretize<MIPS, W><<<ctas, W * 32, smem, stream>>>(P, g);
+}
+
 // Shared by hc_discretize (rasters only) and the frame launch (rasters + mips 0..5 +
 // patch bytes + valid-range partials + the render's tile-queue histograms).
 int hc::discretize_launch(const HcCascadeRaster* cascades, int n_cascades, const HcGrid* grid, float sentinel,
@@ -1032,22 +1056,13 @@ int hc::discretize_launch(const HcCascadeRaster* cascades, int n_cascades, const
         }
     }
     const int ctas = P.n_blocks + order_ctas;
+    const bool six = P.n_blocks >= DISC_WIDE_BLOCKS || (mips && mips->throughput);
     if (mips) {
-        constexpr size_t smem = disc_smem_bytes<true>();
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_discretize<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
-        k_discretize<true><<<ctas, 256, smem, stream>>>(P, *grid);
+        if (six) launch_disc<true, 6>(P, *grid, ctas, stream);
+        else launch_disc<true, 8>(P, *grid, ctas, stream);
     } else {
-        constexpr size_t smem = disc_smem_bytes<false>();
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_discretize<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
-        k_discretize<false><<<ctas, 256, smem, stream>>>(P, *grid);
+        if (six) launch_disc<false, 6>(P, *grid, ctas, stream);
+        else launch_disc<false, 8>(P, *grid, ctas, stream);
     }
     return cuda_status("hc_discretize");
 }

@@ -34,6 +34,7 @@ struct DiscMipJob {
     int32_t full;                            // write every level under blocks outside the mask
     float* xchg;                             // sharded frame: exchange buffer (heightcast.h HcFootprint), or NULL
     const HcFootprint* fp;                   // with xchg: the strips' ground wedges
+    int32_t throughput;                      // frames overlap: use the throughput CTA shape
 };
 
 int discretize_launch(const HcCascadeRaster* cascades, int n_cascades, const HcGrid* grid, float sentinel,

@@ -71,16 +71,20 @@ __device__ __forceinline__ unsigned warp_bucket_counts(const int b[PER], int lan
     return mine;
 }
 
-// histogram of chunk `chunk`; the whole CTA (blockDim.x == T) calls it
+// histogram of chunk `chunk`; the whole CTA (blockDim.x >= T, a multiple of 32) calls
+// it, threads 0..T-1 count (ORDER_CHUNK must be a multiple of T)
 template <int T>
 __device__ __forceinline__ void order_count_chunk(const int32_t* __restrict__ cost, int32_t* __restrict__ order,
                                                   int n_tiles, int chunk) {
+    static_assert(ORDER_CHUNK % T == 0 && T % 32 == 0, "order chunk must split into whole warps");
     constexpr int PER = ORDER_CHUNK / T, W = T / 32;
     __shared__ unsigned wh[W][33];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int b[PER];
-    load_buckets<T>(cost, n_tiles, chunk, b);
-    wh[warp][lane] = warp_bucket_counts<PER>(b, lane);
+    if ((int)threadIdx.x < T) {
+        int b[PER];
+        load_buckets<T>(cost, n_tiles, chunk, b);
+        wh[warp][lane] = warp_bucket_counts<PER>(b, lane);
+    }
     __syncthreads();
     if (threadIdx.x < 32) {
         unsigned t = 0;

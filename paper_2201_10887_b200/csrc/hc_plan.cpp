@@ -835,6 +835,7 @@ static int frame_launch(int stages, const HcPlan* plan, const HcCamera* cam, con
     }
     dm.xchg = xchg;
     dm.fp = fp;
+    dm.throughput = buf->throughput;
     if (xchg && (!fp || nlev < 7)) {
         hc::set_error("hc_frame_stage: sharded frames need a footprint and R >= 34 (got R = %d)", R);
         return HC_EINVAL;
