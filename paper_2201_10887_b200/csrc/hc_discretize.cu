@@ -54,12 +54,16 @@ namespace hc {
 constexpr double NEG_HALF_LOG2E = -0.72134752044448170368;
 // r2 >= 12.25 (3.5 sigma, rbf.py:29-32) <=> q = r2 * NEG_HALF_LOG2E <= Q_CUT
 constexpr float Q_CUT = (float)(12.25 * NEG_HALF_LOG2E);
-#ifndef DISC_STAGE_PAIRS
-#define DISC_STAGE_PAIRS 80        // record pairs per warp buffer: ~64 KB shared memory per 6-warp CTA
-                                   // (3 per SM), the rest of the 256 KB stays L1 for the lookups and
-                                   // gathers (measured 32-128 pairs at 4/5/6/8 warps: DESIGN.md §4)
+// record pairs per warp staging buffer, shared by up to STAGE_GROUPS cells, per CTA
+// shape: 64 for 4-warp CTAs (~41 KB shared memory, 4 per SM), 96 for 8-warp CTAs
+// (~85 KB, 2 per SM); the rest of the 256 KB stays L1 for the lookups and gathers
+// (measured 32-128 pairs at 4/5/6/7/8 warps per CTA: DESIGN.md §4)
+#ifndef DISC_STAGE_PAIRS_WIDE
+#define DISC_STAGE_PAIRS_WIDE 64
 #endif
-constexpr int STAGE_PAIRS = DISC_STAGE_PAIRS;   // record pairs per warp buffer, shared by up to STAGE_GROUPS cells
+#ifndef DISC_STAGE_PAIRS_LONE
+#define DISC_STAGE_PAIRS_LONE 96
+#endif
 #ifndef DISC_GATHER_PREFETCH
 #define DISC_GATHER_PREFETCH 1     // gathered units: 0 none, 1 per-lane line prefetches, 2 bulk prefetch
 #endif
@@ -68,33 +72,48 @@ constexpr int STAGE_PAIRS = DISC_STAGE_PAIRS;   // record pairs per warp buffer,
 #endif
 constexpr int STAGE_GROUPS = DISC_STAGE_GROUPS;
 // Two CTA shapes (the same 32x32 blocks, the same per-texel arithmetic and results):
-//  * 6 warps, 3 CTAs per SM -- while one CTA waits at a barrier for its longest unit
-//    two others issue: 5-8 % faster on the 4K configs (32k blocks) and for
-//    overlapping frames (render_frames);
-//  * 8 warps, 2 CTAs per SM -- faster for a lone frame of a few thousand blocks (C1,
-//    C2), whose last wave of CTAs sets the time.
+//  * 4 warps, 4 CTAs per SM, 64 staged pairs -- while one CTA waits at a barrier for
+//    its longest unit three others issue, and ~41 KB of shared memory per CTA leaves
+//    L1 to the lookups: 8-15 % faster on the 4K configs (32k blocks) and for
+//    overlapping frames of >= 4k blocks (render_frames);
+//  * 8 warps, 2 CTAs per SM, 96 staged pairs -- faster for a lone frame of a few
+//    thousand blocks (C1, C2), whose last wave of CTAs sets the time;
+//  * 6 warps, 3 CTAs per SM, 80 staged pairs -- small launches of overlapping frames
+//    (C1 in render_frames).
 #ifndef DISC_WIDE_BLOCKS
-#define DISC_WIDE_BLOCKS 16384     // blocks per launch from which the 6-warp shape is used
+#define DISC_WIDE_BLOCKS 16384     // blocks per launch from which the 4-warp shape is used
 #endif
-constexpr int MINB_FOR(int warps) { return warps == 6 ? 3 : 2; }
+#ifndef DISC_WIDE_WARPS
+#define DISC_WIDE_WARPS 4
+#endif
+#ifndef DISC_WIDE_MINB
+#define DISC_WIDE_MINB 4
+#endif
+// third shape: small launches of overlapping frames (C1 in render_frames)
+constexpr int MID_WARPS = 6;
+constexpr int MINB_FOR(int warps) { return warps == DISC_WIDE_WARPS ? DISC_WIDE_MINB : (warps == MID_WARPS ? 3 : 2); }
+constexpr int SP_FOR(int warps) {
+    return warps == DISC_WIDE_WARPS ? DISC_STAGE_PAIRS_WIDE : (warps == MID_WARPS ? 80 : DISC_STAGE_PAIRS_LONE);
+}
 // threads of an extra CTA that count a tile-queue histogram chunk (a divisor of ORDER_CHUNK)
 constexpr int ORDER_THREADS_FOR(int threads) { return threads >= 256 ? 256 : (threads >= 128 ? 128 : 64); }
 constexpr int BLK = 32;            // texels per block side (= level-5 mip node)
 constexpr int TILE_LEVELS = 6;     // mip levels 0..5 reduced per block
 constexpr int QUAD = 10;           // float4 per quad of record pairs (heightcast.h HcGrid.rec)
-// pairs per group slot and chunk for ng groups: floor(STAGE_PAIRS / ng) rounded down to whole quads
-__host__ __device__ constexpr int group_chunk(int ng) { return (STAGE_PAIRS / ng) & ~3; }
+// pairs per group slot and chunk for ng groups: floor(SP / ng) rounded down to whole quads
+template <int SP>
+__host__ __device__ constexpr int group_chunk(int ng) { return (SP / ng) & ~3; }
 // float4 per buffer: max over ng of ng * (chg / 4 * QUAD + 1) (one odd pad per group slot
 // spreads the groups' slots over the shared-memory banks)
+template <int SP>
 constexpr int stage_f4() {
     int m = 0;
     for (int ng = 1; ng <= STAGE_GROUPS; ++ng) {
-        const int v = ng * (group_chunk(ng) / 4 * QUAD + 1);
+        const int v = ng * (group_chunk<SP>(ng) / 4 * QUAD + 1);
         m = v > m ? v : m;
     }
     return m;
 }
-constexpr int STAGE_F4 = stage_f4();
 
 // ---------------------------------------------------------------------------
 // TMA bulk copy + mbarrier (sm_90+ PTX; SASS UBLKCP / SYNCS)
@@ -390,7 +409,7 @@ __device__ __forceinline__ int unit_texel(int u, int lane) {
     return lane == 0 ? 32 * REG + 32 : -1;          // halo corner
 }
 
-template <int REG>
+template <int REG, int SP>
 __device__ __forceinline__ Unit plan_unit(int u, int lane, const int* s_cell, const int2* s_pr) {
     Unit U;
     U.e = unit_texel<REG>(u, lane);
@@ -421,7 +440,7 @@ __device__ __forceinline__ Unit plan_unit(int u, int lane, const int* s_cell, co
     U.chg = 0;
     U.nchunks = 0;
     if (U.ng > 0 && rem == 0u) {
-        U.chg = group_chunk(U.ng);
+        U.chg = group_chunk<SP>(U.ng);
         const int maxq = (int)__reduce_max_sync(FULL, (unsigned)(lane < U.ng ? U.gn : 0));
         const int cq = U.chg >> 2;
         U.nchunks = (maxq + cq - 1) / cq;
@@ -444,6 +463,8 @@ __global__ void __launch_bounds__(DISC_WARPS * 32, MINB_FOR(DISC_WARPS)) k_discr
     constexpr int NU = MIPS ? 35 : 32;             // units of 32 texels
     constexpr int DISC_THREADS = DISC_WARPS * 32;
     constexpr int ORDER_THREADS = ORDER_THREADS_FOR(DISC_THREADS);
+    constexpr int SP = SP_FOR(DISC_WARPS);
+    constexpr int STAGE_F4 = stage_f4<SP>();
     const unsigned FULL = 0xffffffffu;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -675,14 +696,14 @@ __global__ void __launch_bounds__(DISC_WARPS * 32, MINB_FOR(DISC_WARPS)) k_discr
     int u = grab();
     Unit U;
     if (u < NU) {
-        U = plan_unit<REG>(u, lane, s_cell, s_pr);
+        U = plan_unit<REG, SP>(u, lane, s_cell, s_pr);
         if (U.nchunks) issue(U, 0, buf);
     }
     while (u < NU) {
         const int un = grab();
         Unit N;
         N.nchunks = 0;
-        if (un < NU) N = plan_unit<REG>(un, lane, s_cell, s_pr);
+        if (un < NU) N = plan_unit<REG, SP>(un, lane, s_cell, s_pr);
         // lane's texel: anchors (consumed after the records) and offset to its cell centre
         float at = 0.f, ad = 0.f;
         float2 nrx = make_float2(0.f, 0.f), nry = nrx;
@@ -903,16 +924,20 @@ constexpr size_t disc_smem_bytes() {
     constexpr size_t REG = MIPS ? BLK + 1 : BLK;
     constexpr size_t NT = REG * REG;
     constexpr size_t head = ((4 * ((NT + 1) & ~(size_t)1) + 16 * NT + NT) + 127) & ~(size_t)127;
-    constexpr size_t stage = DISC_WARPS * 2 * 16 * STAGE_F4 + DISC_WARPS * 2 * 8;
+    constexpr size_t stage = DISC_WARPS * 2 * 16 * stage_f4<SP_FOR(DISC_WARPS)>() + DISC_WARPS * 2 * 8;
     return head + stage;
 }
-static_assert(6 * 2 * 16 * STAGE_F4 >= 2 * 2 * BLK * (BLK + 1) * 4, "mip levels alias the staging area");
+static_assert(DISC_WIDE_WARPS * 2 * 16 * stage_f4<SP_FOR(DISC_WIDE_WARPS)>() >= 2 * 2 * BLK * (BLK + 1) * 4 &&
+                  8 * 2 * 16 * stage_f4<SP_FOR(8)>() >= 2 * 2 * BLK * (BLK + 1) * 4,
+              "mip levels alias the staging area");
+template <int SP>
 constexpr bool stage_fits() {
     for (int ng = 1; ng <= STAGE_GROUPS; ++ng)
-        if (ng * (group_chunk(ng) / 4 * QUAD + 1) > STAGE_F4 || group_chunk(ng) < 4) return false;
+        if (ng * (group_chunk<SP>(ng) / 4 * QUAD + 1) > stage_f4<SP>() || group_chunk<SP>(ng) < 4) return false;
     return true;
 }
-static_assert(stage_fits(), "a chunk of STAGE_GROUPS groups overflows the warp buffer");
+static_assert(stage_fits<SP_FOR(DISC_WIDE_WARPS)>() && stage_fits<SP_FOR(8)>() && stage_fits<SP_FOR(MID_WARPS)>(),
+              "a chunk of STAGE_GROUPS groups overflows the warp buffer");
 
 // float64 Eq. 2 at arbitrary points (rbf.py:87-130 per segment)
 __global__ void k_eval_points(HcGrid g, const double* __restrict__ px, const double* __restrict__ py,
@@ -1056,12 +1081,14 @@ int hc::discretize_launch(const HcCascadeRaster* cascades, int n_cascades, const
         }
     }
     const int ctas = P.n_blocks + order_ctas;
-    const bool six = P.n_blocks >= DISC_WIDE_BLOCKS || (mips && mips->throughput);
+    const bool overlap = mips && mips->throughput;
+    const bool wide = P.n_blocks >= DISC_WIDE_BLOCKS || (overlap && P.n_blocks >= DISC_WIDE_BLOCKS / 4);
     if (mips) {
-        if (six) launch_disc<true, 6>(P, *grid, ctas, stream);
+        if (wide) launch_disc<true, DISC_WIDE_WARPS>(P, *grid, ctas, stream);
+        else if (overlap) launch_disc<true, MID_WARPS>(P, *grid, ctas, stream);
         else launch_disc<true, 8>(P, *grid, ctas, stream);
     } else {
-        if (six) launch_disc<false, 6>(P, *grid, ctas, stream);
+        if (wide) launch_disc<false, DISC_WIDE_WARPS>(P, *grid, ctas, stream);
         else launch_disc<false, 8>(P, *grid, ctas, stream);
     }
     return cuda_status("hc_discretize");
