@@ -55,11 +55,11 @@ constexpr double NEG_HALF_LOG2E = -0.72134752044448170368;
 // r2 >= 12.25 (3.5 sigma, rbf.py:29-32) <=> q = r2 * NEG_HALF_LOG2E <= Q_CUT
 constexpr float Q_CUT = (float)(12.25 * NEG_HALF_LOG2E);
 // record pairs per warp staging buffer, shared by up to STAGE_GROUPS cells, per CTA
-// shape: 64 for 4-warp CTAs (~41 KB shared memory, 4 per SM), 96 for 8-warp CTAs
+// shape: 72 for 4-warp CTAs (~44 KB shared memory, 4 per SM), 96 for 8-warp CTAs
 // (~85 KB, 2 per SM); the rest of the 256 KB stays L1 for the lookups and gathers
 // (measured 32-128 pairs at 4/5/6/7/8 warps per CTA: DESIGN.md §4)
 #ifndef DISC_STAGE_PAIRS_WIDE
-#define DISC_STAGE_PAIRS_WIDE 64
+#define DISC_STAGE_PAIRS_WIDE 72
 #endif
 #ifndef DISC_STAGE_PAIRS_LONE
 #define DISC_STAGE_PAIRS_LONE 96
