@@ -97,7 +97,7 @@ def summarise(rep, tag, config, work=None):
            "lsu_pipe": "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
            "occupancy": "sm__warps_active.avg.pct_of_peak_sustained_active",
            "l1_hit": "l1tex__t_sector_hit_rate.pct", "l2_hit": "lts__t_sector_hit_rate.pct"}
-    cfg = {"_source": os.path.basename(rep)}
+    cfg = {"_source": f"{tag}.md (from {os.path.basename(rep)})"}
     seen = set()
     for short, r in kernels:
         key = KERNEL_KEY.get(short.replace("void ", "").split("<")[0].strip())
