@@ -480,6 +480,33 @@ def test_sharded_strips_need_six_mip_levels(cuda):
     assert np.array_equal(img, full)
 
 
+@pytest.mark.parametrize("i", range(8))
+def test_sharded_strips_random_poses(cuda, i):
+    """Sharded screen strips at the stress poses (grazing, below-terrain, outside the
+    domain, straight down -- where a strip may reach the whole plane), random strip
+    counts and uneven cuts, 1-6 cascades: the emulated ranks' image equals the
+    single-GPU frame bit for bit."""
+    from paper_2201_10887_b200 import multi, render_frame
+    from paper_2201_10887_b200.cascade import CameraView
+    from paper_2201_10887_b200.rbf import RbfParams
+    from paper_2201_10887_b200.render import CascadeSettings, FrameConfig
+    cfg, g, t, _ = _config_inputs("C2")
+    rng = np.random.default_rng(77 + i)
+    eye, look, up, fov = _random_poses()[2 * i]
+    W, H = 480, 270
+    cam = CameraView(eye=eye, look_dir=look, up=up, fov_y=fov, aspect=W / H, near_clip=1.0, far_clip=6000.0)
+    st = CascadeSettings(resolution=(256, 512, 300)[i % 3], count=1 + (i * 5) % 6)
+    fc = FrameConfig(width=W, height=H, camera=cam)
+    full = render_frame(fc, g, t, RbfParams(sigma=cfg.sigma), st)
+    if not full.visible:
+        pytest.skip("nothing visible from this pose")
+    world = int(rng.integers(2, 7))
+    cuts = sorted(set(int(c) for c in rng.integers(1, W // 8, world - 1) * 8))
+    rects = [(a, b) for a, b in zip([0] + cuts, cuts + [W])]
+    img, _ = multi.render_strips_one_gpu(fc, g, t, None, st, len(rects), rects)
+    assert np.array_equal(img, full.pixels), (i, rects)
+
+
 def test_division_selftest(cuda):
     """The traversal's hoisted float64 division equals IEEE a / b on 2^28 operand pairs."""
     import torch
