@@ -1008,10 +1008,14 @@ extern "C" int hc_visibility_mask(const HcCascadeRaster* c, hc_stream_t stream) 
 template <bool MIPS, int W>
 static void launch_disc(const DiscParams& P, const HcGrid& g, int ctas, cudaStream_t stream) {
     constexpr size_t smem = disc_smem_bytes<MIPS, W>();
-    static bool attr = false;          // per process; the attribute is per function
-    if (!attr) {
+    // the attribute belongs to the function in each device's context: set it once per
+    // device (a benign race if two host threads get here first at the same time)
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !attr[dev]) {
         cudaFuncSetAttribute(k_discretize<MIPS, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
+        if (dev >= 0 && dev < 64) attr[dev] = true;
     }
     k_discretize<MIPS, W><<<ctas, W * 32, smem, stream>>>(P, g);
 }
