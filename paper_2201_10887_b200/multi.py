@@ -2,7 +2,9 @@
 
 * camera batches (C4): views are independent; rank r renders views
   r, r+N, r+2N, ... of a batch against the grid resident in its own HBM.
-  `shard_views` assigns them; no data-path collective, weak scaling.
+  `shard_views` assigns them; no data-path collective, weak scaling;
+  `gather_views` collects a batch's frames on one rank when the caller wants
+  them there (one gather per round of views).
 * screen strips (C5): every rank plans the SAME full-view cascades (the host
   planner is deterministic) and traces only its vertical strip of pixels
   (`HcRenderArgs.x0..x1`).  Each rank builds its own cascades: it discretizes
@@ -32,6 +34,33 @@ def shard_views(n_views: int, world: int, rank: int) -> list[int]:
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad world/rank")
     return list(range(rank, n_views, world))
+
+
+def gather_views(frames, n_views: int, rank: int, world: int, group=None, dst: int = 0):
+    """Collect a view batch on `dst`: rank r holds the (H, W, 3) uint8 frames of views
+    shard_views(n_views, world, r), in that order.  One gather per round of views
+    (round i: view i*world + r from every rank; ranks without a view that round send
+    a zero frame); returns the list of n_views frames on `dst`, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+    mine = shard_views(n_views, world, rank)
+    if len(frames) != len(mine):
+        raise ValueError(f"rank {rank} holds {len(frames)} frames for {len(mine)} views")
+    if not frames:
+        raise ValueError("every rank needs at least one view (n_views >= world)")
+    like = frames[0]
+    out = [None] * n_views if rank == dst else None
+    rounds = (n_views + world - 1) // world
+    for i in range(rounds):
+        send = frames[i] if i < len(frames) else torch.zeros_like(like)
+        parts = [torch.empty_like(like) for _ in range(world)] if rank == dst else None
+        dist.gather(send.contiguous(), parts, dst=dst, group=group)
+        if rank == dst:
+            for r, p in enumerate(parts):
+                v = i * world + r
+                if v < n_views:
+                    out[v] = p
+    return out
 
 
 def screen_strips(width: int, world: int, weights=None) -> list[tuple[int, int]]:

@@ -58,13 +58,19 @@ def _worker(rank, world, port, q):
     xchg = torch.from_numpy(np.where(mine, truth, -np.inf).astype(np.float32))
     multi.all_reduce_max(xchg)
     xchg_ok = bool(np.array_equal(xchg.numpy(), truth))
+    # C4 view batch: 5 views over the ranks, gathered to rank 0 in view order
+    n_views = 5
+    mine = multi.shard_views(n_views, world, rank)
+    frames = [torch.full((3, 4, 3), v, dtype=torch.uint8) for v in mine]
+    views = multi.gather_views(frames, n_views, rank, world)
+    views_ok = views is None if rank else [int(f[0, 0, 0]) for f in views] == list(range(n_views))
     # weak-scaling timing reduction used by bench.py: max over ranks
     t = torch.tensor([float(rank + 1)])
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
-        q.put((bool(np.array_equal(out.numpy(), full)) and xchg_ok, float(t.item())))
+        q.put((bool(np.array_equal(out.numpy(), full)) and xchg_ok and views_ok, float(t.item())))
     else:
-        assert out is None and xchg_ok
+        assert out is None and xchg_ok and views_ok
     dist.barrier()
     dist.destroy_process_group()
 
