@@ -118,7 +118,7 @@ def test_gpu_tile_painter_matches_host(cuda, kind, seed, cells, max_depth):
     dev_index = g.device_tile_index(cuda)
     assert dev_index is not None, "grid was not painted on the GPU"
     host = synth.generate_synthetic(kind, seed, cells, max_depth=max_depth, native_paint=False).tile_index
-    assert torch.equal(dev_index, torch.from_numpy(np.ascontiguousarray(host)).to(cuda))
+    assert torch.equal(dev_index, torch.from_numpy(np.array(host, copy=True)).to(cuda))
     assert np.array_equal(g.tile_index, host)                   # the lazy host download
     assert g.device_view(cuda).tile_index.data_ptr() == dev_index.data_ptr()
 
