@@ -67,6 +67,9 @@ constexpr float Q_CUT = (float)(12.25 * NEG_HALF_LOG2E);
 #ifndef DISC_GATHER_PREFETCH
 #define DISC_GATHER_PREFETCH 1     // gathered units: 0 none, 1 per-lane line prefetches, 2 bulk prefetch
 #endif
+#ifndef DISC_RECORD_EVICT_FIRST
+#define DISC_RECORD_EVICT_FIRST 0  // L2 evict-first hint on influence-record reads
+#endif
 #ifndef DISC_STAGE_GROUPS
 #define DISC_STAGE_GROUPS 12       // cells per staged unit (8 / 12 / 16 measured: 12 best)
 #endif
@@ -139,10 +142,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // global -> shared bulk copy (bytes multiple of 16, both addresses 16-byte aligned),
 // completion counted on `bar`
 __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+#if DISC_RECORD_EVICT_FIRST
+    // records are read once per unit: mark them first to leave L2 so they do not push
+    // out the rasters and pyramids the render reads next
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_u32(smem)),
+        "l"(gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+#else
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(smem)),
                  "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
+#endif
 }
 // order this thread's earlier generic-proxy accesses of shared memory before later
 // async-proxy (TMA) writes to it
@@ -381,7 +396,7 @@ __device__ __forceinline__ void quad4_global(Acc& A, float2 nrx, float2 nry, flo
                                              const float4* __restrict__ q) {
     float4 v[QUAD];
 #pragma unroll
-    for (int i = 0; i < QUAD; ++i) v[i] = __ldg(q + i);
+    for (int i = 0; i < QUAD; ++i) v[i] = DISC_RECORD_EVICT_FIRST ? __ldcs(q + i) : __ldg(q + i);
     pair2(A, nrx, nry, nrem, v[0], v[4], make_float2(v[8].x, v[8].y));
     pair2(A, nrx, nry, nrem, v[1], v[5], make_float2(v[8].z, v[8].w));
     pair2(A, nrx, nry, nrem, v[2], v[6], make_float2(v[9].x, v[9].y));
