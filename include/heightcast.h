@@ -423,6 +423,11 @@ int hc_selftest_division(uint64_t n, uint64_t seed, uint64_t *mismatches, hc_str
  * where it differs from the reference's sequence alone (counts[0]), hits
  * (counts[1]) and misses starting below the patch (counts[2]); device uint64[3]. */
 int hc_selftest_patch(uint64_t n, uint64_t seed, uint64_t *counts, hc_stream_t stream);
+/* Self-test of the render's certified slab pre-test: counts generated cases (many
+ * aimed within ulps of a slab corner or edge) that it calls empty while the exact
+ * slab setup does not miss (counts[0], must be 0), pre-test empties (counts[1]) and
+ * exact misses (counts[2]); device uint64[3]. */
+int hc_selftest_slab(uint64_t n, uint64_t seed, uint64_t *counts, hc_stream_t stream);
 /* Measurement only: reads `bytes` of device memory `passes` times (L2-resident when
  * bytes < L2) in one launch; bench.py times it for the L2 roofline. */
 int hc_bench_l2_read(const void *buf, size_t bytes, int passes, float *sink, hc_stream_t stream);

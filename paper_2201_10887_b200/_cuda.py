@@ -33,7 +33,7 @@ EXPORTS = ("hc_py_hypot", "hc_visible_hull", "hc_clip_cascades", "hc_fit_layout"
            "hc_discretize", "hc_maxmip_workspace_bytes", "hc_maxmip", "hc_render", "hc_render_tiles",
            "hc_render_order_words", "hc_traverse_batch", "hc_eval_points", "hc_influence_workspace_bytes",
            "hc_influence_build", "hc_frame_launch", "hc_frame_xchg_floats", "hc_frame_stage",
-           "hc_selftest_division", "hc_selftest_patch", "hc_bench_l2_read", "hc_ahf_parse",
+           "hc_selftest_division", "hc_selftest_patch", "hc_selftest_slab", "hc_bench_l2_read", "hc_ahf_parse",
            "hc_paint_tiles", "hc_paint_tiles_device")
 HC_MAX_HULL = 64
 
@@ -219,6 +219,7 @@ def lib():
     L.hc_render_order_words.argtypes = [C.c_int] * 4
     L.hc_selftest_division.argtypes = [C.c_uint64, C.c_uint64, _vp, _vp]
     L.hc_selftest_patch.argtypes = [C.c_uint64, C.c_uint64, _vp, _vp]
+    L.hc_selftest_slab.argtypes = [C.c_uint64, C.c_uint64, _vp, _vp]
     L.hc_bench_l2_read.argtypes = [_vp, C.c_size_t, C.c_int, _vp, _vp]
     L.hc_eval_points.argtypes = [C.POINTER(HcGrid), _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
     L.hc_ahf_parse.argtypes = [C.c_char_p, _i64, C.POINTER(HcAhfInfo), _vp, _i64]

@@ -392,6 +392,21 @@ def test_patch_early_rejection_selftest(cuda):
     assert bad == 0
 
 
+def test_slab_pretest_selftest(cuda):
+    """The render's certified slab pre-test never calls a slab empty that the exact
+    setup (traverse_raster's divisions) does not miss, on 2^26 generated cases --
+    half of them aimed within ulps of a slab corner or edge, with zero and tiny
+    direction components -- and it catches most exact misses."""
+    import torch
+    from paper_2201_10887_b200 import _cuda
+    cnt = torch.zeros(3, dtype=torch.int64, device=cuda)
+    _cuda.check(_cuda.lib().hc_selftest_slab(1 << 26, 91, cnt.data_ptr(), _cuda.stream_ptr()), "selftest")
+    bad, pre, exact = (int(x) for x in cnt.tolist())
+    print(f"slab selftest: {bad} false empties, {pre} pre-test empties of {exact} exact misses")
+    assert bad == 0
+    assert exact > 1000 and pre > 0.5 * exact
+
+
 def _random_poses():
     """Camera poses over the C2 grid (domain [0, 2048]^2, heights ~12-100 m) that
     stress the traversal's exact shortcuts: axis-aligned and integer-coordinate
