@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define HC_ABI_VERSION 6
+#define HC_ABI_VERSION 7
 #define HC_MAX_EDGES 32      /* polygon edges per cascade mask          */
 #define HC_MAX_CASCADES 8    /* K (the reference hard-codes 3)           */
 #define HC_MAX_LEVELS 20     /* max-mip levels (R <= 2^19)               */

@@ -17,7 +17,7 @@ LIB_DIR = os.path.join(PKG_DIR, "_lib")
 LIB_PATH = os.environ.get("HC_LIB_PATH") or os.path.join(LIB_DIR, "libheightcast_cuda.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 
-HC_ABI_VERSION = 6
+HC_ABI_VERSION = 7
 HC_MAX_EDGES = 32
 HC_MAX_CASCADES = 8
 HC_MAX_LEVELS = 20
